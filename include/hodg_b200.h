@@ -1,0 +1,148 @@
+/* hodg_b200 -- C ABI of the B200 (sm_100a) DG Euler residual library.
+ *
+ * Drop-in boundary for the reference's hot path (arXiv 2209.01877, package
+ * `hodg`).  Each entry point replaces one piece of the reference's kernel
+ * seam, cited below:
+ *
+ *   hodg_face_flux      <- _KERNELS[dtype].flux_pass     hodg/dg.py:240-351
+ *                          (wrapper face_flux_pass       hodg/dg.py:594-621)
+ *   hodg_elem_stage     <- _KERNELS[dtype].rhs_pass      hodg/dg.py:353-460
+ *                          fused with _axpy_state / _combine_state
+ *                                                        hodg/timestepping.py:165-180
+ *                          (wrapper accumulate_rhs       hodg/dg.py:624-649)
+ *   hodg_local_dt       <- _dt_pass / local_dt_field     hodg/timestepping.py:105-147
+ *   hodg_min_reduce_f64 <- min_reduce                    hodg/timestepping.py:150-162
+ *   hodg_residual_l2    <- residual_l2                   hodg/timestepping.py:208-211
+ *   hodg_rcm            <- cuthill_mckee / rcm           hodg/renumber.py:171-208
+ *   hodg_err_decode     <- _raise_face_error / _raise_cell_error
+ *                                                        hodg/dg.py:537-546
+ *
+ * Conventions (inherited from the reference seam):
+ *  - plain pointers and sizes; every buffer is DEVICE memory owned by the
+ *    caller; the library never allocates on the hot path;
+ *  - calls are asynchronous on the given stream (cudaStream_t passed as
+ *    void*); kernels never fail on inadmissible states, they record the
+ *    first (smallest) offending face / cell id in a device error word
+ *    (uint32[4], reset with hodg_err_reset) that the host reads once per step;
+ *  - return value: HODG_OK, HODG_EINVAL (bad argument), HODG_ECUDA (launch
+ *    error), HODG_ENODEV (no sm_100 device).
+ *
+ * Data layout in HBM (N elements, F faces, nb modes, 5 variables):
+ *  - state / residual: (N, 5, nb) float64, row stride rs = 5*nb rounded up
+ *    to an even count, in the reference-element monomial basis (see
+ *    DESIGN.md; hodg_modal_transform converts to/from the reference's
+ *    physical Taylor basis);
+ *  - face flux buffer: (F, 5, nqf) at kernel precision (the reference's
+ *    FaceFluxBuffer.inviscid, hodg/dg.py:86-92, transposed);
+ *  - geometry: see hodg_mesh_desc.
+ */
+#ifndef HODG_B200_H
+#define HODG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HODG_OK 0
+#define HODG_EINVAL 2
+#define HODG_ECUDA 3
+#define HODG_ENODEV 4
+
+/* boundary kinds, hodg/physics.py:47-50 */
+#define HODG_BC_INTERIOR 0
+#define HODG_BC_FAR_FIELD 1
+#define HODG_BC_SLIP_WALL 2
+#define HODG_BC_NO_SLIP_WALL 3
+
+#define HODG_FLUX_ROE 0
+#define HODG_FLUX_LLF 1
+
+/* kernel precision: 64 = FP64 everywhere; 32 = FP32 traces / flux /
+ * quadrature with FP64 state, accumulation, mass solve and RK update */
+#define HODG_PREC_F64 64
+#define HODG_PREC_MIXED 32
+
+/* element geometry record, 16 doubles per element */
+#define HODG_EGEO_STRIDE 16 /* Jinv[9] row-major, fc[4] = sgn*area/vol, h, vol, pad */
+#define HODG_ECONV_STRIDE 18 /* A = J/h [9], A^-1 [9] (modal transforms) */
+
+typedef struct {
+    int64_t n_elems;
+    int64_t n_faces;
+    int order;        /* 0..3 */
+    int flux_kind;    /* HODG_FLUX_ROE | HODG_FLUX_LLF */
+    double gamma;
+    double qinf[5];   /* far-field state (conserved) */
+    const double* egeo;      /* (N, 16) */
+    const double* econv;     /* (N, 18) */
+    const int32_t* efaces;   /* (N, 4) face id of local face s (opposite vertex s) */
+    const int32_t* fcells;   /* (F, 2) left, right (-1 at boundary) */
+    const int32_t* finfo;    /* (F,) slotL | slotR << 2 | bc << 4 */
+    const double* fnrm;      /* (F, 4) unit normal left->right, pad */
+} hodg_mesh_desc;
+
+typedef struct hodg_mesh hodg_mesh;
+
+/* RK stage: out = a*u0 + b*(us + dt*R(us))       (combine = 0)
+ *           out = 0.5*((u0 + us) + dt*R(us))      (combine = 1, Heun final stage)
+ *           no state update                       (combine = -1, residual only) */
+typedef struct {
+    const double* us;   /* stage state (N, rs) */
+    const double* u0;   /* RK base state, may be NULL when combine == 0 and a == 0 */
+    double* out;        /* new state; may alias us (never u0 unless u0 == us is dead) */
+    double* res;        /* residual dU/dt (N, rs), NULL to skip */
+    double a, b;
+    int combine;
+    int dt_is_vector;        /* dt: device scalar (0) or per-element vector (1) */
+    const double* dt;
+    double* norm_partial;    /* (n_blocks, 5) partial sums of vol*res_0^2, NULL to skip */
+    unsigned long long* dt_next;   /* atomic min of the new state's CFL dt (double bits), NULL to skip */
+    double* dt_vec_out;      /* per-element CFL dt of the new state, NULL to skip */
+    unsigned long long* dt_reset;  /* set to +inf by this launch (another step's dt slot), NULL to skip */
+    double cfl;
+} hodg_stage_args;
+
+int hodg_version(void);
+int hodg_device_ok(void);
+int hodg_mesh_create(const hodg_mesh_desc* desc, hodg_mesh** out);
+int hodg_mesh_destroy(hodg_mesh* mesh);
+int hodg_state_row_stride(int order);  /* rs */
+int hodg_n_basis(int order);
+int hodg_n_face_points(int order);
+int hodg_n_vol_points(int order);
+int64_t hodg_stage_blocks(const hodg_mesh* mesh, int prec); /* rows of norm_partial */
+
+int hodg_face_flux(const hodg_mesh* mesh, int prec, const double* state, void* face_buf, uint32_t* err,
+                   void* stream);
+int hodg_elem_stage(const hodg_mesh* mesh, int prec, const void* face_buf, const hodg_stage_args* args,
+                    uint32_t* err, void* stream);
+int hodg_local_dt(const hodg_mesh* mesh, const double* state, double cfl, double* dt_vec_out,
+                  unsigned long long* dt_min, uint32_t* err, void* stream);
+int hodg_norm_finalize(const double* partial, int64_t n_blocks, double* out5, void* stream);
+int hodg_residual_l2(const hodg_mesh* mesh, const double* res, double* scratch, double* out5, void* stream);
+int hodg_min_reduce_f64(const double* x, int64_t n, double* scratch, double* out, void* stream);
+int hodg_dt_fill(unsigned long long* slot, double value, void* stream);
+int hodg_modal_transform(const hodg_mesh* mesh, int to_reference, const double* in, double* out, void* stream);
+int hodg_err_reset(uint32_t* err, void* stream);
+/* decode a host copy of the error word: returns 0 (ok), 1 face, 2 volume cell, 3 cell mean; *id = first id */
+int hodg_err_decode(const uint32_t* err_host, int64_t* id);
+
+/* Device Reverse Cuthill-McKee (bit-exact with hodg/renumber.py:171-208).
+ * indptr (n+1), indices (2E) int64 CSR, neighbour lists ascending (as
+ * AdjacencyGraph.from_edges builds them).  forward[old] = new,
+ * inverse[new] = old.  work: caller-provided device scratch of
+ * hodg_rcm_work_bytes(n, nnz) bytes. */
+int64_t hodg_rcm_work_bytes(int64_t n, int64_t nnz);
+int hodg_rcm(int64_t n, const int64_t* indptr, const int64_t* indices, int64_t* forward, int64_t* inverse,
+             void* work, void* stream);
+
+/* number of kernels this library launched since load (for gpu_launches) */
+int64_t hodg_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HODG_B200_H */

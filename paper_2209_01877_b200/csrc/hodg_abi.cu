@@ -1,0 +1,270 @@
+// C ABI of libhodg_b200 (include/hodg_b200.h): argument checks, dispatch on
+// the polynomial order, and the order-independent kernels (deterministic
+// reductions, dt slots, error words).
+#include <atomic>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+
+#include "../../include/hodg_b200.h"
+#include "hodg_common.cuh"
+
+#define DECL_ORDER(P)                                                                                          \
+    int hodg_launch_face_p##P(const hodg_mesh_desc&, int, const double*, void*, uint32_t*, cudaStream_t);     \
+    int hodg_launch_elem_p##P(const hodg_mesh_desc&, int, const void*, const hodg_stage_args&, uint32_t*,      \
+                              cudaStream_t);                                                                   \
+    int hodg_launch_dt_p##P(const hodg_mesh_desc&, const double*, double, double*, unsigned long long*,        \
+                            uint32_t*, cudaStream_t);                                                          \
+    int hodg_launch_modal_p##P(const hodg_mesh_desc&, int, const double*, double*, cudaStream_t);             \
+    int64_t hodg_elem_blocks_p##P(int64_t);
+DECL_ORDER(0)
+DECL_ORDER(1)
+DECL_ORDER(2)
+DECL_ORDER(3)
+
+int hodg_rcm_impl(int64_t n, const int64_t* indptr, const int64_t* indices, int64_t* forward, int64_t* inverse,
+                  void* work, cudaStream_t st, int64_t* launches);
+int64_t hodg_rcm_work_bytes_impl(int64_t n, int64_t nnz);
+
+struct hodg_mesh {
+    hodg_mesh_desc d;
+};
+
+static std::atomic<int64_t> g_launches{0};
+
+static inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+namespace {
+
+constexpr int NB_TAB[4] = {1, 4, 10, 20};
+constexpr int NQV_TAB[4] = {1, 4, 14, 24};
+constexpr int NQF_TAB[4] = {1, 6, 7, 15};
+
+inline int rs_of(int p) { return (5 * NB_TAB[p] + 1) & ~1; }
+
+// fixed-shape deterministic reductions ------------------------------------
+constexpr int RT = 256;
+
+__global__ void norm_partial_kernel(const double* __restrict__ res, const double* __restrict__ egeo, int64_t n,
+                                    int rs, double* __restrict__ partial) {
+    __shared__ double sm[5][RT];
+    const int64_t c = int64_t(blockIdx.x) * RT + threadIdx.x;
+    double v5[5] = {0, 0, 0, 0, 0};
+    if (c < n) {
+        const double vol = egeo[c * 16 + 14];
+        const int nb = rs >= 100 ? 20 : (rs >= 50 ? 10 : (rs >= 20 ? 4 : 1));
+        for (int v = 0; v < 5; ++v) {
+            const double r = res[c * rs + v * nb];
+            v5[v] = vol * r * r;
+        }
+    }
+    for (int v = 0; v < 5; ++v) sm[v][threadIdx.x] = v5[v];
+    __syncthreads();
+    for (int w = RT / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w)
+            for (int v = 0; v < 5; ++v) sm[v][threadIdx.x] += sm[v][threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x < 5) partial[int64_t(blockIdx.x) * 5 + threadIdx.x] = sm[threadIdx.x][0];
+}
+
+// one CTA: thread k sums rows k, k+RT, ... in order, then a fixed tree
+__global__ void norm_finalize_kernel(const double* __restrict__ partial, int64_t nblk, double* __restrict__ out5) {
+    __shared__ double sm[5][RT];
+    double s[5] = {0, 0, 0, 0, 0};
+    for (int64_t b = threadIdx.x; b < nblk; b += RT)
+        for (int v = 0; v < 5; ++v) s[v] += partial[b * 5 + v];
+    for (int v = 0; v < 5; ++v) sm[v][threadIdx.x] = s[v];
+    __syncthreads();
+    for (int w = RT / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w)
+            for (int v = 0; v < 5; ++v) sm[v][threadIdx.x] += sm[v][threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x < 5) out5[threadIdx.x] = sqrt(sm[threadIdx.x][0]);
+}
+
+__global__ void min_partial_kernel(const double* __restrict__ x, int64_t n, double* __restrict__ out) {
+    __shared__ double sm[RT];
+    double m = __longlong_as_double(0x7FF0000000000000ll);
+    for (int64_t i = int64_t(blockIdx.x) * RT + threadIdx.x; i < n; i += int64_t(gridDim.x) * RT) m = fmin(m, x[i]);
+    sm[threadIdx.x] = m;
+    __syncthreads();
+    for (int w = RT / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) sm[threadIdx.x] = fmin(sm[threadIdx.x], sm[threadIdx.x + w]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[blockIdx.x] = sm[0];
+}
+
+__global__ void fill_u64_kernel(unsigned long long* slot, unsigned long long bits) { *slot = bits; }
+
+}  // namespace
+
+extern "C" {
+
+int hodg_version(void) { return 1; }
+
+int hodg_device_ok(void) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    cudaDeviceProp p;
+    if (cudaGetDeviceProperties(&p, dev) != cudaSuccess) return 0;
+    return p.major == 10 ? 1 : 0;
+}
+
+int hodg_state_row_stride(int order) { return (order < 0 || order > 3) ? -1 : rs_of(order); }
+int hodg_n_basis(int order) { return (order < 0 || order > 3) ? -1 : NB_TAB[order]; }
+int hodg_n_face_points(int order) { return (order < 0 || order > 3) ? -1 : NQF_TAB[order]; }
+int hodg_n_vol_points(int order) { return (order < 0 || order > 3) ? -1 : NQV_TAB[order]; }
+
+int hodg_mesh_create(const hodg_mesh_desc* desc, hodg_mesh** out) {
+    if (!desc || !out) return HODG_EINVAL;
+    if (desc->order < 0 || desc->order > 3 || desc->n_elems <= 0 || desc->n_faces <= 0) return HODG_EINVAL;
+    if (desc->n_elems > 0x7FFFFFFFll || desc->n_faces > 0x7FFFFFFFll) return HODG_EINVAL;
+    if (!desc->egeo || !desc->econv || !desc->efaces || !desc->fcells || !desc->finfo || !desc->fnrm)
+        return HODG_EINVAL;
+    if (desc->flux_kind != HODG_FLUX_ROE && desc->flux_kind != HODG_FLUX_LLF) return HODG_EINVAL;
+    if (!(desc->gamma > 1.0)) return HODG_EINVAL;
+    hodg_mesh* m = new (std::nothrow) hodg_mesh;
+    if (!m) return HODG_EINVAL;
+    m->d = *desc;
+    *out = m;
+    return HODG_OK;
+}
+
+int hodg_mesh_destroy(hodg_mesh* mesh) {
+    delete mesh;
+    return HODG_OK;
+}
+
+int64_t hodg_stage_blocks(const hodg_mesh* mesh, int prec) {
+    (void)prec;
+    if (!mesh) return -1;
+    switch (mesh->d.order) {
+        case 0: return hodg_elem_blocks_p0(mesh->d.n_elems);
+        case 1: return hodg_elem_blocks_p1(mesh->d.n_elems);
+        case 2: return hodg_elem_blocks_p2(mesh->d.n_elems);
+        default: return hodg_elem_blocks_p3(mesh->d.n_elems);
+    }
+}
+
+int hodg_face_flux(const hodg_mesh* mesh, int prec, const double* state, void* face_buf, uint32_t* err,
+                   void* stream) {
+    if (!mesh || !state || !face_buf) return HODG_EINVAL;
+    if (prec != HODG_PREC_F64 && prec != HODG_PREC_MIXED) return HODG_EINVAL;
+    g_launches++;
+    switch (mesh->d.order) {
+        case 0: return hodg_launch_face_p0(mesh->d, prec, state, face_buf, err, S(stream));
+        case 1: return hodg_launch_face_p1(mesh->d, prec, state, face_buf, err, S(stream));
+        case 2: return hodg_launch_face_p2(mesh->d, prec, state, face_buf, err, S(stream));
+        default: return hodg_launch_face_p3(mesh->d, prec, state, face_buf, err, S(stream));
+    }
+}
+
+int hodg_elem_stage(const hodg_mesh* mesh, int prec, const void* face_buf, const hodg_stage_args* a, uint32_t* err,
+                    void* stream) {
+    if (!mesh || !face_buf || !a || !a->us) return HODG_EINVAL;
+    if (prec != HODG_PREC_F64 && prec != HODG_PREC_MIXED) return HODG_EINVAL;
+    if (a->combine < -1 || a->combine > 1) return HODG_EINVAL;
+    if (a->combine >= 0 && (!a->out || !a->dt)) return HODG_EINVAL;
+    if (a->combine == 1 && !a->u0) return HODG_EINVAL;
+    if (a->combine == 0 && a->a != 0.0 && !a->u0) return HODG_EINVAL;
+    if (a->combine < 0 && !a->res && !a->norm_partial) return HODG_EINVAL;
+    g_launches++;
+    switch (mesh->d.order) {
+        case 0: return hodg_launch_elem_p0(mesh->d, prec, face_buf, *a, err, S(stream));
+        case 1: return hodg_launch_elem_p1(mesh->d, prec, face_buf, *a, err, S(stream));
+        case 2: return hodg_launch_elem_p2(mesh->d, prec, face_buf, *a, err, S(stream));
+        default: return hodg_launch_elem_p3(mesh->d, prec, face_buf, *a, err, S(stream));
+    }
+}
+
+int hodg_local_dt(const hodg_mesh* mesh, const double* state, double cfl, double* dt_vec_out,
+                  unsigned long long* dt_min, uint32_t* err, void* stream) {
+    if (!mesh || !state || !(cfl > 0.0)) return HODG_EINVAL;
+    g_launches++;
+    switch (mesh->d.order) {
+        case 0: return hodg_launch_dt_p0(mesh->d, state, cfl, dt_vec_out, dt_min, err, S(stream));
+        case 1: return hodg_launch_dt_p1(mesh->d, state, cfl, dt_vec_out, dt_min, err, S(stream));
+        case 2: return hodg_launch_dt_p2(mesh->d, state, cfl, dt_vec_out, dt_min, err, S(stream));
+        default: return hodg_launch_dt_p3(mesh->d, state, cfl, dt_vec_out, dt_min, err, S(stream));
+    }
+}
+
+int hodg_modal_transform(const hodg_mesh* mesh, int to_reference, const double* in, double* out, void* stream) {
+    if (!mesh || !in || !out || in == out) return HODG_EINVAL;
+    g_launches++;
+    switch (mesh->d.order) {
+        case 0: return hodg_launch_modal_p0(mesh->d, to_reference, in, out, S(stream));
+        case 1: return hodg_launch_modal_p1(mesh->d, to_reference, in, out, S(stream));
+        case 2: return hodg_launch_modal_p2(mesh->d, to_reference, in, out, S(stream));
+        default: return hodg_launch_modal_p3(mesh->d, to_reference, in, out, S(stream));
+    }
+}
+
+int hodg_norm_finalize(const double* partial, int64_t n_blocks, double* out5, void* stream) {
+    if (!partial || !out5 || n_blocks <= 0) return HODG_EINVAL;
+    g_launches++;
+    norm_finalize_kernel<<<1, RT, 0, S(stream)>>>(partial, n_blocks, out5);
+    return cudaGetLastError() == cudaSuccess ? HODG_OK : HODG_ECUDA;
+}
+
+int hodg_residual_l2(const hodg_mesh* mesh, const double* res, double* scratch, double* out5, void* stream) {
+    if (!mesh || !res || !scratch || !out5) return HODG_EINVAL;
+    const int64_t n = mesh->d.n_elems;
+    const int64_t nblk = (n + RT - 1) / RT;
+    g_launches += 2;
+    norm_partial_kernel<<<unsigned(nblk), RT, 0, S(stream)>>>(res, mesh->d.egeo, n, rs_of(mesh->d.order), scratch);
+    norm_finalize_kernel<<<1, RT, 0, S(stream)>>>(scratch, nblk, out5);
+    return cudaGetLastError() == cudaSuccess ? HODG_OK : HODG_ECUDA;
+}
+
+int hodg_min_reduce_f64(const double* x, int64_t n, double* scratch, double* out, void* stream) {
+    if (!x || !scratch || !out || n <= 0) return HODG_EINVAL;
+    int64_t nblk = (n + RT - 1) / RT;
+    if (nblk > 1024) nblk = 1024;
+    g_launches += 2;
+    min_partial_kernel<<<unsigned(nblk), RT, 0, S(stream)>>>(x, n, scratch);
+    min_partial_kernel<<<1, RT, 0, S(stream)>>>(scratch, nblk, out);
+    return cudaGetLastError() == cudaSuccess ? HODG_OK : HODG_ECUDA;
+}
+
+int hodg_dt_fill(unsigned long long* slot, double value, void* stream) {
+    if (!slot) return HODG_EINVAL;
+    unsigned long long bits;
+    std::memcpy(&bits, &value, 8);
+    g_launches++;
+    fill_u64_kernel<<<1, 1, 0, S(stream)>>>(slot, bits);
+    return cudaGetLastError() == cudaSuccess ? HODG_OK : HODG_ECUDA;
+}
+
+int hodg_err_reset(uint32_t* err, void* stream) {
+    if (!err) return HODG_EINVAL;
+    return cudaMemsetAsync(err, 0xFF, 4 * sizeof(uint32_t), S(stream)) == cudaSuccess ? HODG_OK : HODG_ECUDA;
+}
+
+int hodg_err_decode(const uint32_t* err, int64_t* id) {
+    if (!err) return HODG_EINVAL;
+    for (int k = 0; k < 3; ++k)
+        if (err[k] != HODG_ERR_NONE) {
+            if (id) *id = int64_t(err[k]);
+            return k + 1;
+        }
+    if (id) *id = -1;
+    return 0;
+}
+
+int64_t hodg_rcm_work_bytes(int64_t n, int64_t nnz) { return hodg_rcm_work_bytes_impl(n, nnz); }
+
+int hodg_rcm(int64_t n, const int64_t* indptr, const int64_t* indices, int64_t* forward, int64_t* inverse,
+             void* work, void* stream) {
+    int64_t launches = 0;
+    const int rc = hodg_rcm_impl(n, indptr, indices, forward, inverse, work, S(stream), &launches);
+    g_launches += launches;
+    return rc;
+}
+
+int64_t hodg_launch_count(void) { return g_launches.load(); }
+
+}  // extern "C"

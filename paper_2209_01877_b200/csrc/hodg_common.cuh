@@ -1,0 +1,256 @@
+// Shared device code for the tetrahedral DG Euler residual (sm_100a).
+//
+// Point physics restated from the reference's scalar ops
+// (hodg/physics.py:158-344) for 5 conserved variables (rho, rho u, rho v,
+// rho w, E): primitive recovery, the Roe flux with the Harten-Hyman entropy
+// fix (delta = 0.05 a), the LLF flux, and the far-field / slip / no-slip
+// boundary states.  Templated on the arithmetic type so the mixed-precision
+// path runs genuine FP32 flux arithmetic.
+//
+// Also: PTX wrappers for mbarrier + cp.async.bulk (the 1-D TMA engine) used
+// to stage element tiles in shared memory.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/hodg_b200.h"
+
+#define HODG_ERR_NONE 0xFFFFFFFFu
+
+namespace hodg {
+
+// ---------------------------------------------------------------------------
+// TMA bulk copies and mbarriers (PTX ISA: cp.async.bulk, mbarrier)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// global -> shared, completion counted on `bar` (bytes % 16 == 0, 16B aligned)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// shared -> global (bulk group); caller waits with bulk_wait_read()
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+// make generic-proxy smem writes visible to the async (TMA) proxy
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------
+// error words: err[0] first inadmissible face, err[1] first inadmissible
+// volume point's cell, err[2] first inadmissible cell mean (dt pass)
+
+__device__ __forceinline__ void flag(uint32_t* err, int which, uint32_t id) {
+    if (err) atomicMin(err + which, id);
+}
+
+// ---------------------------------------------------------------------------
+// point physics
+
+template <typename T>
+struct K {
+    static constexpr T one = T(1), half = T(0.5), two = T(2), quarter = T(0.25), efix = T(0.05), zero = T(0);
+};
+
+// primitive (u, v, w, p) from conserved; hodg/physics.py:159-165
+template <typename T>
+__device__ __forceinline__ T prim(const T q[5], T g, T& u, T& v, T& w) {
+    T ri = K<T>::one / q[0];
+    u = q[1] * ri;
+    v = q[2] * ri;
+    w = q[3] * ri;
+    return (g - K<T>::one) * (q[4] - K<T>::half * q[0] * (u * u + v * v + w * w));
+}
+
+// Roe flux with Harten-Hyman entropy fix; hodg/physics.py:177-250 (3D)
+template <typename T>
+__device__ __forceinline__ bool roe(const T qL[5], const T qR[5], const T n[3], T g, T f[5]) {
+    const T one = K<T>::one, half = K<T>::half, two = K<T>::two;
+    if (!(qL[0] > K<T>::zero) || !(qR[0] > K<T>::zero)) return false;
+    T uL, vL, wL, uR, vR, wR;
+    T pL = prim(qL, g, uL, vL, wL);
+    T pR = prim(qR, g, uR, vR, wR);
+    if (!(pL > K<T>::zero) || !(pR > K<T>::zero)) return false;
+    const T nx = n[0], ny = n[1], nz = n[2];
+    T vnL = uL * nx + vL * ny + wL * nz;
+    T vnR = uR * nx + vR * ny + wR * nz;
+    T sL = sqrt(qL[0]);
+    T sR = sqrt(qR[0]);
+    T di = one / (sL + sR);
+    T ut = (sL * uL + sR * uR) * di;
+    T vt = (sL * vL + sR * vR) * di;
+    T wt = (sL * wL + sR * wR) * di;
+    T HL = (qL[4] + pL) / qL[0];
+    T HR = (qR[4] + pR) / qR[0];
+    T Ht = (sL * HL + sR * HR) * di;
+    T ke = half * (ut * ut + vt * vt + wt * wt);
+    T a2 = (g - one) * (Ht - ke);
+    if (!(a2 > K<T>::zero)) return false;
+    T a = sqrt(a2);
+    T rt = sL * sR;
+    T unt = ut * nx + vt * ny + wt * nz;
+    T dr = qR[0] - qL[0];
+    T dp = pR - pL;
+    T du = uR - uL, dv = vR - vL, dw = wR - wL;
+    T dun = vnR - vnL;
+    T l1 = fabs(unt - a), l2 = fabs(unt), l4 = fabs(unt + a);
+    T delta = K<T>::efix * a;
+    if (l1 < delta) l1 = half * (l1 * l1 / delta + delta);
+    if (l4 < delta) l4 = half * (l4 * l4 / delta + delta);
+    T ia2 = one / a2;
+    T rad = rt * a * dun;
+    T a1 = (dp - rad) * (half * ia2);
+    T a4 = (dp + rad) * (half * ia2);
+    T a2w = dr - dp * ia2;
+    T w1 = l1 * a1, w4 = l4 * a4;
+    T d0 = w1 + l2 * a2w + w4;
+    T d1 = w1 * (ut - a * nx) + l2 * (a2w * ut + rt * (du - dun * nx)) + w4 * (ut + a * nx);
+    T d2 = w1 * (vt - a * ny) + l2 * (a2w * vt + rt * (dv - dun * ny)) + w4 * (vt + a * ny);
+    T d3 = w1 * (wt - a * nz) + l2 * (a2w * wt + rt * (dw - dun * nz)) + w4 * (wt + a * nz);
+    T dE = w1 * (Ht - a * unt) + l2 * (a2w * ke + rt * (ut * du + vt * dv + wt * dw - unt * dun)) +
+           w4 * (Ht + a * unt);
+    f[0] = half * (qL[0] * vnL + qR[0] * vnR) - half * d0;
+    f[1] = half * (qL[1] * vnL + pL * nx + qR[1] * vnR + pR * nx) - half * d1;
+    f[2] = half * (qL[2] * vnL + pL * ny + qR[2] * vnR + pR * ny) - half * d2;
+    f[3] = half * (qL[3] * vnL + pL * nz + qR[3] * vnR + pR * nz) - half * d3;
+    f[4] = half * ((qL[4] + pL) * vnL + (qR[4] + pR) * vnR) - half * dE;
+    return true;
+}
+
+// local Lax-Friedrichs (Rusanov) flux
+template <typename T>
+__device__ __forceinline__ bool llf(const T qL[5], const T qR[5], const T n[3], T g, T f[5]) {
+    if (!(qL[0] > K<T>::zero) || !(qR[0] > K<T>::zero)) return false;
+    T uL, vL, wL, uR, vR, wR;
+    T pL = prim(qL, g, uL, vL, wL);
+    T pR = prim(qR, g, uR, vR, wR);
+    if (!(pL > K<T>::zero) || !(pR > K<T>::zero)) return false;
+    T vnL = uL * n[0] + vL * n[1] + wL * n[2];
+    T vnR = uR * n[0] + vR * n[1] + wR * n[2];
+    T sl = fabs(vnL) + sqrt(g * pL / qL[0]);
+    T sr = fabs(vnR) + sqrt(g * pR / qR[0]);
+    T lam = sl > sr ? sl : sr;
+    T FL[5] = {qL[0] * vnL, qL[1] * vnL + pL * n[0], qL[2] * vnL + pL * n[1], qL[3] * vnL + pL * n[2],
+               (qL[4] + pL) * vnL};
+    T FR[5] = {qR[0] * vnR, qR[1] * vnR + pR * n[0], qR[2] * vnR + pR * n[1], qR[3] * vnR + pR * n[2],
+               (qR[4] + pR) * vnR};
+#pragma unroll
+    for (int v = 0; v < 5; ++v) f[v] = K<T>::half * (FL[v] + FR[v]) - K<T>::half * lam * (qR[v] - qL[v]);
+    return true;
+}
+
+// boundary states; hodg/physics.py:292-344 with a 3-vector tangential velocity
+template <typename T>
+__device__ __forceinline__ void bstate(int kind, const T q[5], const T n[3], const T qf[5], T g, T out[5]) {
+    const T one = K<T>::one, two = K<T>::two, half = K<T>::half;
+    if (kind == HODG_BC_FAR_FIELD) {
+        T ui, vi, wi, uf, vf, wf;
+        T pi = prim(q, g, ui, vi, wi);
+        T pf = prim(qf, g, uf, vf, wf);
+        T ai = sqrt(g * pi / q[0]);
+        T af = sqrt(g * pf / qf[0]);
+        T uni = ui * n[0] + vi * n[1] + wi * n[2];
+        T unf = uf * n[0] + vf * n[1] + wf * n[2];
+        if (uni >= ai) {
+#pragma unroll
+            for (int v = 0; v < 5; ++v) out[v] = q[v];
+            return;
+        }
+        if (unf <= -af) {
+#pragma unroll
+            for (int v = 0; v < 5; ++v) out[v] = qf[v];
+            return;
+        }
+        T gm1i = one / (g - one);
+        T rplus = uni + two * ai * gm1i;
+        T rminus = unf - two * af * gm1i;
+        T unb = half * (rplus + rminus);
+        T ab = K<T>::quarter * (g - one) * (rplus - rminus);
+        if (!(ab > K<T>::zero)) {
+#pragma unroll
+            for (int v = 0; v < 5; ++v) out[v] = qf[v];
+            return;
+        }
+        T s, utx, uty, utz;
+        if (unb > K<T>::zero) {
+            s = pi / pow(q[0], g);
+            utx = ui - uni * n[0];
+            uty = vi - uni * n[1];
+            utz = wi - uni * n[2];
+        } else {
+            s = pf / pow(qf[0], g);
+            utx = uf - unf * n[0];
+            uty = vf - unf * n[1];
+            utz = wf - unf * n[2];
+        }
+        T rb = pow(ab * ab / (g * s), gm1i);
+        T pb = rb * ab * ab / g;
+        T ub = utx + unb * n[0], vb = uty + unb * n[1], wb = utz + unb * n[2];
+        out[0] = rb;
+        out[1] = rb * ub;
+        out[2] = rb * vb;
+        out[3] = rb * wb;
+        out[4] = pb * gm1i + half * rb * (ub * ub + vb * vb + wb * wb);
+    } else if (kind == HODG_BC_SLIP_WALL) {
+        T un2 = two * (q[1] * n[0] + q[2] * n[1] + q[3] * n[2]);
+        out[0] = q[0];
+        out[1] = q[1] - un2 * n[0];
+        out[2] = q[2] - un2 * n[1];
+        out[3] = q[3] - un2 * n[2];
+        out[4] = q[4];
+    } else {  // no-slip (also any unknown code, as the reference)
+        out[0] = q[0];
+        out[1] = -q[1];
+        out[2] = -q[2];
+        out[3] = -q[3];
+        out[4] = q[4];
+    }
+}
+
+}  // namespace hodg

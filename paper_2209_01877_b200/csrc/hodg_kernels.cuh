@@ -1,0 +1,555 @@
+// Per-order tetrahedral DG kernels.  Included once per polynomial order by
+// hodg_p{0..3}.cu after the order's constant tables, with
+//   ORDER, NB, NQV, NQF and the table macros VB_D/VB_F, VD_D/VD_F,
+//   FB_D/FB_F, FG_D/FG_F, MINV_T, MEAN_T
+// defined.  See DESIGN.md for the formulation: every element works in the
+// reference-element monomial basis m_i(eta), so the reference's per-cell
+// tables (hodg/geometry.py:33-51) collapse into compile-time constants and
+// the per-element data is 16 doubles (J^-1, sgn*area/vol per face, h, vol).
+
+#include "hodg_common.cuh"
+
+#define HODG_CAT_(a, b) a##b
+#define HODG_CAT(a, b) HODG_CAT_(a, b)
+#define TAB(NAME, T, k) (sizeof(T) == 8 ? (T)HODG_CAT(NAME, _D)[(k)] : (T)HODG_CAT(NAME, _F)[(k)])
+
+namespace hodg {
+namespace HODG_CAT(ord, ORDER) {
+
+constexpr int RS = (5 * NB + 1) & ~1;        // state row stride (doubles)
+constexpr int NG = (NQF > 8) ? 2 : 1;        // face qp groups per side thread
+constexpr int QPT = (NQF + NG - 1) / NG;     // face qps per phase-1 thread
+constexpr int FACE_THREADS = 128;
+constexpr int FT = FACE_THREADS / (2 * NG);  // faces per CTA
+constexpr int FBS = NQF * NB + 1;            // padded per-slot stride of the smem trace table
+constexpr int E = (ORDER >= 3) ? 16 : (ORDER == 2 ? 32 : 64);  // elements per CTA
+constexpr int ETHREADS = 5 * E;
+constexpr int XS = 15;                        // smem slot per (element, qp): 5 traces -> 15 contravariant fluxes
+
+__host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+__host__ __device__ constexpr size_t cmax(size_t a, size_t b) { return a > b ? a : b; }
+
+// exponent d of monomial i in the graded order (degree, then descending x,
+// then descending y): the reference's `_EXPONENTS` order (hodg/basis.py:21) in 3D
+__host__ __device__ constexpr int expt(int i, int d) {
+    int k = 0, base = 0;
+    while (base + (k + 1) * (k + 2) / 2 <= i) {
+        base += (k + 1) * (k + 2) / 2;
+        ++k;
+    }
+    int r = i - base, a = k;
+    while (r >= k - a + 1) {
+        r -= k - a + 1;
+        --a;
+    }
+    const int b = k - a - r;
+    return d == 0 ? a : (d == 1 ? b : k - a - b);
+}
+
+template <typename T>
+__host__ __device__ constexpr size_t face_smem_bytes() {
+    return align16(16 + 4 * FBS * sizeof(T)) +
+           align16(cmax(size_t(2 * FT) * RS * sizeof(double), size_t(2 * FT) * NQF * 5 * sizeof(T)));
+}
+
+template <typename T>
+__host__ __device__ constexpr size_t elem_smem_bytes() {
+    return 16 + size_t(E) * RS * 8 + size_t(E) * 16 * 8 + size_t(E) * 16 + size_t(E) * 10 * 8 +
+           size_t(NQV) * E * XS * sizeof(T) + 16;
+}
+
+// ---------------------------------------------------------------------------
+// Face kernel: hodg/dg.py:240-351.  One CTA = FT faces.
+//  phase 0: each (face, side) thread bulk-copies its element's state row
+//           (TMA, cp.async.bulk) into shared memory;
+//  phase 1: thread (face, side, qp-group) evaluates the side's traces at the
+//           face quadrature points (reference-basis values of its local face
+//           slot, staged in smem; coefficients reused across qps, basis values
+//           across the 5 variables);
+//  phase 2: thread (face, qp) closes boundary faces with the BC state and
+//           evaluates the Roe / LLF flux, writing H[f][v][q].
+template <typename T>
+__global__ void __launch_bounds__(FACE_THREADS) face_flux_kernel(const hodg_mesh_desc m,
+                                                                 const double* __restrict__ state,
+                                                                 T* __restrict__ hbuf, uint32_t* __restrict__ err) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+    T* fbt = reinterpret_cast<T*>(smem + 16);
+    double* rows = reinterpret_cast<double*>(smem + align16(16 + 4 * FBS * sizeof(T)));
+    T* trs = reinterpret_cast<T*>(rows);  // aliases rows after phase 1
+
+    const int t = threadIdx.x;
+    const int64_t f0 = int64_t(blockIdx.x) * FT;
+    const int nf = int(min(int64_t(FT), m.n_faces - f0));
+    const int side = t / (FT * NG);
+    const int rem = t - side * FT * NG;
+    const int lf = rem / NG;
+    const int g = rem - lf * NG;
+
+    int64_t elem = -1;
+    int slot = 0;
+    if (lf < nf) {
+        elem = m.fcells[2 * (f0 + lf) + side];
+        const int info = m.finfo[f0 + lf];
+        slot = side == 0 ? (info & 3) : ((info >> 2) & 3);
+    }
+    if (t == 0) {
+        mbar_init(bar, FACE_THREADS);
+        mbar_fence_init();
+    }
+    for (int k = t; k < 4 * NQF * NB; k += FACE_THREADS) {
+        const int s = k / (NQF * NB);
+        fbt[s * FBS + (k - s * NQF * NB)] = TAB(FB, T, k);
+    }
+    __syncthreads();
+    double* myrow = rows + size_t(side * FT + lf) * RS;
+    if (g == 0 && elem >= 0) {
+        mbar_arrive_expect_tx(bar, RS * 8);
+        bulk_g2s(myrow, state + elem * RS, RS * 8, bar);
+    } else {
+        mbar_arrive(bar);
+    }
+    mbar_wait(bar, 0);
+
+    T tr[QPT][5];
+#pragma unroll
+    for (int qq = 0; qq < QPT; ++qq)
+#pragma unroll
+        for (int v = 0; v < 5; ++v) tr[qq][v] = T(0);
+    if (elem >= 0) {
+        const T* fb = fbt + slot * FBS;
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+            T c[5];
+#pragma unroll
+            for (int v = 0; v < 5; ++v) c[v] = T(myrow[v * NB + i]);
+#pragma unroll
+            for (int qq = 0; qq < QPT; ++qq) {
+                const int q = g * QPT + qq;
+                if (NG * QPT == NQF || q < NQF) {
+                    const T b = fb[q * NB + i];
+#pragma unroll
+                    for (int v = 0; v < 5; ++v) tr[qq][v] += b * c[v];
+                }
+            }
+        }
+    }
+    __syncthreads();  // every row consumed; reuse the region for traces
+    if (lf < nf) {
+#pragma unroll
+        for (int qq = 0; qq < QPT; ++qq) {
+            const int q = g * QPT + qq;
+            if (NG * QPT == NQF || q < NQF) {
+#pragma unroll
+                for (int v = 0; v < 5; ++v) trs[(size_t(side * FT + lf) * NQF + q) * 5 + v] = tr[qq][v];
+            }
+        }
+    }
+    __syncthreads();
+
+    const T gam = T(m.gamma);
+    for (int p = t; p < nf * NQF; p += FACE_THREADS) {
+        const int lfp = p / NQF;
+        const int q = p - lfp * NQF;
+        const int64_t f = f0 + lfp;
+        const int bc = (m.finfo[f] >> 4) & 15;
+        const double4 nn = reinterpret_cast<const double4*>(m.fnrm)[f];
+        const T n[3] = {T(nn.x), T(nn.y), T(nn.z)};
+        T qL[5], qR[5], h[5];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) qL[v] = trs[(size_t(lfp) * NQF + q) * 5 + v];
+        bool ok = true;
+        if (m.fcells[2 * f + 1] >= 0) {
+#pragma unroll
+            for (int v = 0; v < 5; ++v) qR[v] = trs[(size_t(FT + lfp) * NQF + q) * 5 + v];
+        } else {
+            T u, vv, w;
+            if (!(qL[0] > T(0)) || !(prim(qL, gam, u, vv, w) > T(0))) {
+                ok = false;
+            } else {
+                const T qf[5] = {T(m.qinf[0]), T(m.qinf[1]), T(m.qinf[2]), T(m.qinf[3]), T(m.qinf[4])};
+                bstate(bc, qL, n, qf, gam, qR);
+            }
+        }
+        if (ok) ok = (m.flux_kind == HODG_FLUX_LLF) ? llf(qL, qR, n, gam, h) : roe(qL, qR, n, gam, h);
+        if (!ok) {
+            flag(err, 0, uint32_t(f));
+#pragma unroll
+            for (int v = 0; v < 5; ++v) h[v] = T(0);
+        }
+#pragma unroll
+        for (int v = 0; v < 5; ++v) hbuf[(f * 5 + v) * NQF + q] = h[v];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Element kernel: hodg/dg.py:353-460 fused with the RK stage update
+// (hodg/timestepping.py:165-180) and the next step's CFL dt
+// (hodg/timestepping.py:105-134).  One CTA = E elements, thread (v, e).
+//  phase 0: TMA bulk copies of the state / geometry / face-id tiles;
+//  phase A: thread (v, e): traces of variable v at the NQV volume points;
+//  phase B: thread (e, q): Euler flux, contravariant flux J^-1 F;
+//  phase C: thread (v, e): volume integral, gather of the 4 face fluxes,
+//           reference mass solve (FP64), RK combination, epilogues.
+template <typename T>
+__global__ void __launch_bounds__(ETHREADS) elem_stage_kernel(const hodg_mesh_desc m, const T* __restrict__ hbuf,
+                                                              const hodg_stage_args a, uint32_t* __restrict__ err) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+    double* S = reinterpret_cast<double*>(smem + 16);
+    double* G = S + E * RS;
+    int32_t* FI = reinterpret_cast<int32_t*>(G + E * 16);
+    double* RED = reinterpret_cast<double*>(FI + E * 4);  // [0, 5E): norm terms, [5E, 10E): cell means
+    T* X = reinterpret_cast<T*>(RED + 10 * E);
+    __shared__ unsigned long long blk_dt;
+
+    const int t = threadIdx.x;
+    const int64_t e0 = int64_t(blockIdx.x) * E;
+    const int ne = int(min(int64_t(E), m.n_elems - e0));
+    if (t == 0) {
+        if (a.dt_reset && blockIdx.x == 0) *a.dt_reset = 0x7FF0000000000000ull;
+        blk_dt = 0x7FF0000000000000ull;
+        mbar_init(bar, 1);
+        mbar_fence_init();
+        const uint32_t bs = uint32_t(ne) * RS * 8, bg = uint32_t(ne) * 16 * 8, bf = uint32_t(ne) * 16;
+        mbar_arrive_expect_tx(bar, bs + bg + bf);
+        bulk_g2s(S, a.us + e0 * RS, bs, bar);
+        bulk_g2s(G, m.egeo + e0 * 16, bg, bar);
+        bulk_g2s(FI, m.efaces + e0 * 4, bf, bar);
+    }
+    __syncthreads();
+    mbar_wait(bar, 0);
+
+    const int v = t / E;
+    const int e = t - v * E;
+
+    // phase A: volume traces of variable v
+    if (e < ne) {
+        T c[NB];
+#pragma unroll
+        for (int i = 0; i < NB; ++i) c[i] = T(S[e * RS + v * NB + i]);
+#pragma unroll
+        for (int q = 0; q < NQV; ++q) {
+            T u = T(0);
+#pragma unroll
+            for (int i = 0; i < NB; ++i) u += TAB(VB, T, q * NB + i) * c[i];
+            X[(q * E + e) * XS + v] = u;
+        }
+    }
+    __syncthreads();
+
+    // phase B: flux and contravariant flux at each (element, qp)
+    const T gam = T(m.gamma);
+    for (int p = t; p < E * NQV; p += ETHREADS) {
+        const int q = p / E;
+        const int ee = p - q * E;
+        if (ee >= ne) continue;
+        T* sl = X + (q * E + ee) * XS;
+        T U[5];
+#pragma unroll
+        for (int k = 0; k < 5; ++k) U[k] = sl[k];
+        T u, vv, w;
+        const T pr = (U[0] > T(0)) ? prim(U, gam, u, vv, w) : T(-1);
+        if (!(pr > T(0))) {
+            flag(err, 1, uint32_t(e0 + ee));
+#pragma unroll
+            for (int k = 0; k < XS; ++k) sl[k] = T(0);
+            continue;
+        }
+        const T Hs = U[4] + pr;
+        const T F[3][5] = {{U[1], U[1] * u + pr, U[1] * vv, U[1] * w, Hs * u},
+                           {U[2], U[2] * u, U[2] * vv + pr, U[2] * w, Hs * vv},
+                           {U[3], U[3] * u, U[3] * vv, U[3] * w + pr, Hs * w}};
+        const double* Ji = G + ee * 16;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const T j0 = T(Ji[3 * k]), j1 = T(Ji[3 * k + 1]), j2 = T(Ji[3 * k + 2]);
+#pragma unroll
+            for (int c = 0; c < 5; ++c) sl[k * 5 + c] = j0 * F[0][c] + j1 * F[1][c] + j2 * F[2][c];
+        }
+    }
+    __syncthreads();
+
+    // phase C
+    const int64_t gid = e0 + e;
+    if (e < ne) {
+        T acc[NB];
+#pragma unroll
+        for (int i = 0; i < NB; ++i) acc[i] = T(0);
+#pragma unroll
+        for (int q = 0; q < NQV; ++q) {
+            const T* sl = X + (q * E + e) * XS;
+            const T fd[3] = {sl[v], sl[5 + v], sl[10 + v]};
+#pragma unroll
+            for (int i = 0; i < NB; ++i)
+#pragma unroll
+                for (int d = 0; d < 3; ++d)
+                    if (expt(i, d) > 0) acc[i] += TAB(VD, T, (q * NB + i) * 3 + d) * fd[d];
+        }
+        double accd[NB];
+#pragma unroll
+        for (int i = 0; i < NB; ++i) accd[i] = double(acc[i]);
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            const int64_t f = FI[e * 4 + s];
+            const T* H = hbuf + (f * 5 + v) * NQF;
+            T hq[NQF];
+#pragma unroll
+            for (int q = 0; q < NQF; ++q) hq[q] = __ldg(H + q);
+            T fa[NB];
+#pragma unroll
+            for (int i = 0; i < NB; ++i) fa[i] = T(0);
+#pragma unroll
+            for (int q = 0; q < NQF; ++q)
+#pragma unroll
+                for (int i = 0; i < NB; ++i) fa[i] += TAB(FG, T, (s * NQF + q) * NB + i) * hq[q];
+            const double fc = G[e * 16 + 9 + s];
+#pragma unroll
+            for (int i = 0; i < NB; ++i) accd[i] -= fc * double(fa[i]);
+        }
+        double r[NB];
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+            double z = 0.0;
+#pragma unroll
+            for (int k = 0; k < NB; ++k) z += MINV_T[j * NB + k] * accd[k];
+            r[j] = z;
+        }
+        if (a.res) {
+#pragma unroll
+            for (int j = 0; j < NB; ++j) a.res[gid * RS + v * NB + j] = r[j];
+        }
+        if (a.norm_partial) RED[v * E + e] = G[e * 16 + 14] * r[0] * r[0];
+        if (a.combine >= 0) {
+            const double dt = a.dt_is_vector ? a.dt[gid] : a.dt[0];
+            double mean = 0.0;
+#pragma unroll
+            for (int j = 0; j < NB; ++j) {
+                const double us = S[e * RS + v * NB + j];
+                double o;
+                if (a.combine == 1) {
+                    o = 0.5 * ((a.u0[gid * RS + v * NB + j] + us) + dt * r[j]);
+                } else {
+                    o = a.b * (us + dt * r[j]);
+                    if (a.a != 0.0) o = a.a * a.u0[gid * RS + v * NB + j] + o;
+                }
+                S[e * RS + v * NB + j] = o;
+                mean += MEAN_T[j] * o;
+            }
+            RED[5 * E + v * E + e] = mean;
+        }
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (t == 0 && a.combine >= 0 && ne > 0) bulk_s2g(a.out + e0 * RS, S, uint32_t(ne) * RS * 8);
+    if (a.norm_partial && t < 5) {
+        double s = 0.0;
+        for (int k = 0; k < ne; ++k) s += RED[t * E + k];
+        a.norm_partial[int64_t(blockIdx.x) * 5 + t] = s;
+    }
+    if (a.combine >= 0 && (a.dt_next || a.dt_vec_out) && t < ne) {
+        // CFL dt of the new cell mean (hodg/timestepping.py:121-134), 3D
+        const double m0 = RED[5 * E + t], m1 = RED[6 * E + t], m2 = RED[7 * E + t], m3 = RED[8 * E + t],
+                     m4 = RED[9 * E + t];
+        double dt = 0.0;
+        if (!(m0 > 0.0)) {
+            flag(err, 2, uint32_t(e0 + t));
+        } else {
+            const double u = m1 / m0, vv = m2 / m0, w = m3 / m0;
+            const double p = (m.gamma - 1.0) * (m4 - 0.5 * m0 * (u * u + vv * vv + w * w));
+            if (!(p > 0.0)) {
+                flag(err, 2, uint32_t(e0 + t));
+            } else {
+                const double fac = 2.0 * ORDER + 1.0;
+                const double h = G[t * 16 + 13];
+                const double speed = sqrt(u * u + vv * vv + w * w) + sqrt(m.gamma * p / m0);
+                dt = a.cfl * h / (fac * speed);
+                if (a.dt_next) atomicMin(&blk_dt, static_cast<unsigned long long>(__double_as_longlong(dt)));
+            }
+        }
+        if (a.dt_vec_out) a.dt_vec_out[e0 + t] = dt;
+    }
+    if (a.dt_next) {
+        __syncthreads();
+        if (t == 0) atomicMin(a.dt_next, blk_dt);
+    }
+    if (t == 0 && a.combine >= 0 && ne > 0) bulk_wait_read();
+}
+
+// ---------------------------------------------------------------------------
+// Standalone CFL dt of a state (hodg/timestepping.py:105-147): thread per element.
+__global__ void local_dt_kernel(const hodg_mesh_desc m, const double* __restrict__ state, double cfl,
+                                double* __restrict__ dt_vec, unsigned long long* __restrict__ dt_min,
+                                uint32_t* __restrict__ err) {
+    const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (c >= m.n_elems) return;
+    double mm[5];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) {
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < NB; ++j) s += MEAN_T[j] * state[c * RS + v * NB + j];
+        mm[v] = s;
+    }
+    double dt = 0.0;
+    if (!(mm[0] > 0.0)) {
+        flag(err, 2, uint32_t(c));
+    } else {
+        const double u = mm[1] / mm[0], vv = mm[2] / mm[0], w = mm[3] / mm[0];
+        const double p = (m.gamma - 1.0) * (mm[4] - 0.5 * mm[0] * (u * u + vv * vv + w * w));
+        if (!(p > 0.0)) {
+            flag(err, 2, uint32_t(c));
+        } else {
+            const double speed = sqrt(u * u + vv * vv + w * w) + sqrt(m.gamma * p / mm[0]);
+            dt = cfl * m.egeo[c * 16 + 13] / ((2.0 * ORDER + 1.0) * speed);
+            if (dt_min) atomicMin(dt_min, static_cast<unsigned long long>(__double_as_longlong(dt)));
+        }
+    }
+    if (dt_vec) dt_vec[c] = dt;
+}
+
+// ---------------------------------------------------------------------------
+// Modal transform between the reference's physical Taylor basis b_j(X),
+// X = (x - xc)/h (hodg/basis.py), and the reference-element basis m_i(eta):
+// b_j(A eta) = sum_i T_ij m_i(eta), A = J/h.  to_reference: c' = T c with A;
+// back: c = T(A^-1) c'.  Each column is the product of |alpha_j| linear forms.
+__device__ __forceinline__ int mono_index(int a, int b, int c) {
+    const int k = a + b + c;
+    return k * (k + 1) * (k + 2) / 6 + (k - a) * (k - a + 1) / 2 + (k - a - b);
+}
+
+__global__ void modal_transform_kernel(const hodg_mesh_desc m, int to_reference, const double* __restrict__ in,
+                                       double* __restrict__ out) {
+    const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (c >= m.n_elems) return;
+    double M[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) M[k] = m.econv[c * 18 + (to_reference ? 0 : 9) + k];
+    double o[5][NB];
+#pragma unroll
+    for (int v = 0; v < 5; ++v)
+#pragma unroll
+        for (int i = 0; i < NB; ++i) o[v][i] = 0.0;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+        double poly[NB];
+#pragma unroll
+        for (int i = 0; i < NB; ++i) poly[i] = 0.0;
+        poly[0] = 1.0;
+        int deg = 0;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+#pragma unroll
+            for (int r = 0; r < expt(j, d); ++r) {
+                double np[NB];
+#pragma unroll
+                for (int i = 0; i < NB; ++i) np[i] = 0.0;
+#pragma unroll
+                for (int i = 0; i < NB; ++i) {
+                    if (expt(i, 0) + expt(i, 1) + expt(i, 2) != deg) continue;
+#pragma unroll
+                    for (int mm = 0; mm < 3; ++mm) {
+                        const int tgt = mono_index(expt(i, 0) + (mm == 0), expt(i, 1) + (mm == 1),
+                                                   expt(i, 2) + (mm == 2));
+                        if (tgt < NB) np[tgt] += poly[i] * M[d * 3 + mm];
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < NB; ++i) poly[i] = np[i];
+                ++deg;
+            }
+        }
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+            const double cj = in[c * RS + v * NB + j];
+#pragma unroll
+            for (int i = 0; i < NB; ++i) o[v][i] += poly[i] * cj;
+        }
+    }
+#pragma unroll
+    for (int v = 0; v < 5; ++v)
+#pragma unroll
+        for (int i = 0; i < NB; ++i) out[c * RS + v * NB + i] = o[v][i];
+}
+
+}  // namespace HODG_CAT(ord, ORDER)
+}  // namespace hodg
+
+// ---------------------------------------------------------------------------
+// host launchers for this order (called by hodg_abi.cu)
+
+namespace hodg {
+namespace HODG_CAT(ord, ORDER) {
+
+template <typename T>
+static int launch_face(const hodg_mesh_desc& m, const double* state, void* hbuf, uint32_t* err, cudaStream_t st) {
+    const size_t sm = face_smem_bytes<T>();
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(face_flux_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)) !=
+            cudaSuccess)
+            return HODG_ECUDA;
+        attr = true;
+    }
+    const int64_t nblk = (m.n_faces + FT - 1) / FT;
+    if (nblk > 0)
+        face_flux_kernel<T><<<unsigned(nblk), FACE_THREADS, sm, st>>>(m, state, static_cast<T*>(hbuf), err);
+    return cudaGetLastError() == cudaSuccess ? HODG_OK : HODG_ECUDA;
+}
+
+template <typename T>
+static int launch_elem(const hodg_mesh_desc& m, const void* hbuf, const hodg_stage_args& a, uint32_t* err,
+                       cudaStream_t st) {
+    const size_t sm = elem_smem_bytes<T>();
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(elem_stage_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)) !=
+            cudaSuccess)
+            return HODG_ECUDA;
+        attr = true;
+    }
+    const int64_t nblk = (m.n_elems + E - 1) / E;
+    if (nblk > 0)
+        elem_stage_kernel<T><<<unsigned(nblk), ETHREADS, sm, st>>>(m, static_cast<const T*>(hbuf), a, err);
+    return cudaGetLastError() == cudaSuccess ? HODG_OK : HODG_ECUDA;
+}
+
+}  // namespace HODG_CAT(ord, ORDER)
+}  // namespace hodg
+
+extern "C++" {
+int HODG_CAT(hodg_launch_face_p, ORDER)(const hodg_mesh_desc& m, int prec, const double* state, void* hbuf,
+                                         uint32_t* err, cudaStream_t st) {
+    using namespace hodg::HODG_CAT(ord, ORDER);
+    return prec == HODG_PREC_MIXED ? launch_face<float>(m, state, hbuf, err, st)
+                                   : launch_face<double>(m, state, hbuf, err, st);
+}
+
+int HODG_CAT(hodg_launch_elem_p, ORDER)(const hodg_mesh_desc& m, int prec, const void* hbuf,
+                                         const hodg_stage_args& a, uint32_t* err, cudaStream_t st) {
+    using namespace hodg::HODG_CAT(ord, ORDER);
+    return prec == HODG_PREC_MIXED ? launch_elem<float>(m, hbuf, a, err, st)
+                                   : launch_elem<double>(m, hbuf, a, err, st);
+}
+
+int HODG_CAT(hodg_launch_dt_p, ORDER)(const hodg_mesh_desc& m, const double* state, double cfl, double* dt_vec,
+                                       unsigned long long* dt_min, uint32_t* err, cudaStream_t st) {
+    using namespace hodg::HODG_CAT(ord, ORDER);
+    const int64_t nblk = (m.n_elems + 127) / 128;
+    if (nblk > 0) local_dt_kernel<<<unsigned(nblk), 128, 0, st>>>(m, state, cfl, dt_vec, dt_min, err);
+    return cudaGetLastError() == cudaSuccess ? HODG_OK : HODG_ECUDA;
+}
+
+int HODG_CAT(hodg_launch_modal_p, ORDER)(const hodg_mesh_desc& m, int to_ref, const double* in, double* out,
+                                          cudaStream_t st) {
+    using namespace hodg::HODG_CAT(ord, ORDER);
+    const int64_t nblk = (m.n_elems + 127) / 128;
+    if (nblk > 0) modal_transform_kernel<<<unsigned(nblk), 128, 0, st>>>(m, to_ref, in, out);
+    return cudaGetLastError() == cudaSuccess ? HODG_OK : HODG_ECUDA;
+}
+
+int64_t HODG_CAT(hodg_elem_blocks_p, ORDER)(int64_t n) {
+    using namespace hodg::HODG_CAT(ord, ORDER);
+    return (n + E - 1) / E;
+}
+}

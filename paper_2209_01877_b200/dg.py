@@ -1,0 +1,321 @@
+"""DG spatial operator on the B200: state containers and the residual API.
+
+Keeps the reference's Python surface (`hodg/dg.py:48-99`, `:549-663`):
+`DofState`, `FaceFluxBuffer`, `Residual`, `BoundaryConditions`,
+`project_initial`, `face_flux_pass`, `accumulate_rhs`, `rhs`, `cell_means`.
+State tensors are torch CUDA tensors in the reference's layout
+(n_cells, n_vars, nb) and the reference's physical Taylor basis; the
+kernels work in the reference-element basis (refelem.py) and the wrappers
+convert with `hodg_modal_transform` on the device.
+
+Precision is dispatched on the state dtype as in the reference
+(`hodg/dg.py:496`): float64 runs FP64 kernels, float32 runs the mixed
+kernels (FP32 traces / flux / quadrature, FP64 accumulation and mass
+solve).  Residuals are always float64.
+
+Errors: the kernels never raise; they record the first inadmissible face /
+cell in a device error word that the wrapper reads once per call and turns
+into `AdmissibilityError(..., face|cell, iteration)` (`hodg/dg.py:537-546`).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .geometry import DeviceGeometry, volume_points
+from .mesh import TetMesh
+from .physics import AdmissibilityError, Conserved, GasModel
+from .refelem import ref_tables
+
+__all__ = [
+    "N_VARS",
+    "BoundaryConditions",
+    "DofState",
+    "FaceFluxBuffer",
+    "Residual",
+    "Discretization",
+    "project_initial",
+    "face_flux_pass",
+    "accumulate_rhs",
+    "rhs",
+    "cell_means",
+]
+
+N_VARS = 5
+FLUX_KINDS = {"roe": _lib.FLUX_ROE, "llf": _lib.FLUX_LLF}
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+@dataclass(frozen=True)
+class BoundaryConditions:
+    """Far-field freestream state (hodg/dg.py:48-53) and the interface flux."""
+
+    freestream: Conserved
+    flux: str = "roe"
+
+    def __post_init__(self):
+        if self.flux not in FLUX_KINDS:
+            raise ValueError(f"unknown flux {self.flux!r}; expected 'roe' or 'llf'")
+
+
+@dataclass
+class DofState:
+    """Per-element modal coefficients (n_cells, 5, nb) in the Taylor basis."""
+
+    coeffs: object
+    iteration: int = 0
+
+    @property
+    def dtype(self):
+        return self.coeffs.dtype
+
+    @property
+    def precision_bits(self) -> int:
+        return self.coeffs.element_size() * 8
+
+    @property
+    def n_basis(self) -> int:
+        return self.coeffs.shape[2]
+
+    def copy(self) -> "DofState":
+        return DofState(self.coeffs.clone(), self.iteration)
+
+
+@dataclass
+class FaceFluxBuffer:
+    """Interface flux at each face quadrature point, (n_faces, nqf, 5)."""
+
+    inviscid: object
+
+
+@dataclass
+class Residual:
+    """dQ/dt modal coefficients (n_cells, 5, nb), always float64."""
+
+    res: object
+
+
+class Discretization:
+    """Device handle for one (mesh, geometry, gas, boundary) setup
+    (hodg/dg.py:476-534): the C-ABI mesh descriptor over device geometry,
+    plus the error word and scratch reused across calls."""
+
+    def __init__(self, mesh: TetMesh, geo: DeviceGeometry, gas: GasModel, bcs: BoundaryConditions, device="cuda"):
+        if gas.ivis:
+            raise NotImplementedError("viscous (BR1) terms are not in the B200 path yet; use ivis=0")
+        torch = _torch()
+        self.L = _lib.lib()
+        self.mesh, self.geo, self.gas, self.bcs = mesh, geo, gas, bcs
+        self.device = torch.device(device)
+        self.order = geo.order
+        self.nb = geo.n_basis
+        self.nqf = geo.n_face_points
+        self.rs = int(self.L.hodg_state_row_stride(self.order))
+        self.n = mesh.n_cells
+        self.nf = mesh.n_faces
+        d = geo.device(self.device)
+        self._d = d
+        desc = _lib.MeshDesc()
+        desc.n_elems = self.n
+        desc.n_faces = self.nf
+        desc.order = self.order
+        desc.flux_kind = FLUX_KINDS[bcs.flux]
+        desc.gamma = gas.gamma
+        for i, x in enumerate(bcs.freestream.as_array()):
+            desc.qinf[i] = float(x)
+        desc.egeo = _lib.ptr(d["egeo"])
+        desc.econv = _lib.ptr(d["econv"])
+        desc.efaces = _lib.ptr(d["efaces"])
+        desc.fcells = _lib.ptr(d["fcells"])
+        desc.finfo = _lib.ptr(d["finfo"])
+        desc.fnrm = _lib.ptr(d["fnrm"])
+        self.desc = desc
+        h = C.c_void_p()
+        _lib.check(self.L.hodg_mesh_create(C.byref(desc), C.byref(h)), "hodg_mesh_create")
+        self.handle = h
+        self.err = torch.empty(4, dtype=torch.int32, device=self.device)
+        self.nblk = int(self.L.hodg_stage_blocks(h, 64))
+        self._hbuf = {}
+        self._scratch = torch.empty(max(self.nblk, (self.n + 255) // 256) * 5 + 1024, dtype=torch.float64,
+                                    device=self.device)
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                self.L.hodg_mesh_destroy(self.handle)
+        except Exception:
+            pass
+
+    # -- buffers ---------------------------------------------------------
+    def face_buffer(self, prec):
+        torch = _torch()
+        b = self._hbuf.get(prec)
+        if b is None:
+            dt = torch.float32 if prec == _lib.PREC_MIXED else torch.float64
+            b = torch.empty((self.nf, N_VARS, self.nqf), dtype=dt, device=self.device)
+            self._hbuf[prec] = b
+        return b
+
+    def new_state(self):
+        return _torch().zeros((self.n, self.rs), dtype=_torch().float64, device=self.device)
+
+    # -- basis conversions -------------------------------------------------
+    def to_reference(self, coeffs, out=None):
+        """(n, 5, nb) Taylor coefficients -> (n, rs) reference-basis rows."""
+        torch = _torch()
+        c = torch.as_tensor(coeffs, device=self.device).to(torch.float64)
+        if tuple(c.shape) != (self.n, N_VARS, self.nb):
+            raise ValueError(f"state shape {tuple(c.shape)} != {(self.n, N_VARS, self.nb)}")
+        src = torch.zeros((self.n, self.rs), dtype=torch.float64, device=self.device)
+        src[:, : N_VARS * self.nb] = c.reshape(self.n, -1)
+        out = self.new_state() if out is None else out
+        _lib.check(self.L.hodg_modal_transform(self.handle, 1, _lib.ptr(src), _lib.ptr(out), _lib.stream_ptr()),
+                   "hodg_modal_transform")
+        return out
+
+    def from_reference(self, rows):
+        """(n, rs) reference-basis rows -> (n, 5, nb) Taylor coefficients."""
+        out = self.new_state()
+        _lib.check(self.L.hodg_modal_transform(self.handle, 0, _lib.ptr(rows), _lib.ptr(out), _lib.stream_ptr()),
+                   "hodg_modal_transform")
+        return out[:, : N_VARS * self.nb].reshape(self.n, N_VARS, self.nb)
+
+    # -- kernels -----------------------------------------------------------
+    def reset_errors(self):
+        _lib.check(self.L.hodg_err_reset(_lib.ptr(self.err), _lib.stream_ptr()), "hodg_err_reset")
+
+    def raise_errors(self, iteration=None):
+        """Read the error word (one device sync) and raise the reference's
+        exception for the first flagged face / cell."""
+        host = self.err.cpu().numpy().astype(np.uint32)
+        idv = C.c_int64(-1)
+        kind = self.L.hodg_err_decode(host.ctypes.data_as(C.c_void_p), C.byref(idv))
+        if kind == 1:
+            raise AdmissibilityError("inadmissible face trace", face=int(idv.value), iteration=iteration)
+        if kind == 2:
+            raise AdmissibilityError("inadmissible volume state", cell=int(idv.value), iteration=iteration)
+        if kind == 3:
+            raise AdmissibilityError("inadmissible cell mean", cell=int(idv.value), iteration=iteration)
+
+    def face_flux(self, rows, prec, hbuf=None, stream=None):
+        hbuf = self.face_buffer(prec) if hbuf is None else hbuf
+        _lib.check(self.L.hodg_face_flux(self.handle, prec, _lib.ptr(rows), _lib.ptr(hbuf), _lib.ptr(self.err),
+                                         _lib.stream_ptr(stream)), "hodg_face_flux")
+        return hbuf
+
+    def stage(self, prec, hbuf, args: _lib.StageArgs, stream=None):
+        _lib.check(self.L.hodg_elem_stage(self.handle, prec, _lib.ptr(hbuf), C.byref(args), _lib.ptr(self.err),
+                                          _lib.stream_ptr(stream)), "hodg_elem_stage")
+
+    def residual_rows(self, rows, hbuf, prec, res=None):
+        res = self.new_state() if res is None else res
+        a = _lib.StageArgs()
+        a.us = _lib.ptr(rows)
+        a.res = _lib.ptr(res)
+        a.combine = -1
+        self.stage(prec, hbuf, a)
+        return res
+
+
+def _get_disc(mesh, geo, gas, bcs) -> Discretization:
+    key = (id(mesh), gas, bcs)
+    disc = geo._disc_cache.get(key)
+    if disc is None:
+        disc = Discretization(mesh, geo, gas, bcs)
+        geo._disc_cache[key] = disc
+    return disc
+
+
+def _prec_of(state) -> int:
+    torch = _torch()
+    if state.coeffs.dtype == torch.float64:
+        return _lib.PREC_F64
+    if state.coeffs.dtype == torch.float32:
+        return _lib.PREC_MIXED
+    raise ValueError(f"unsupported precision {state.coeffs.dtype}")
+
+
+def project_initial(mesh: TetMesh, geo: DeviceGeometry, field, gas: GasModel, device="cuda") -> DofState:
+    """L2 projection of a primitive field onto the basis (hodg/dg.py:549-569).
+    `field(x, y, z)` gets flat arrays over all volume quadrature points and
+    returns a Primitive of arrays.  In the reference-element basis the
+    projector is one constant (nb x nqv) matrix for every element."""
+    torch = _torch()
+    t = ref_tables(geo.order)
+    xyz = volume_points(mesh, geo.order)
+    w = field(xyz[..., 0].ravel(), xyz[..., 1].ravel(), xyz[..., 2].ravel())
+    shape = xyz.shape[:2]
+    rho, u, v, ww, p = (np.broadcast_to(np.asarray(a, dtype=np.float64), (shape[0] * shape[1],)).reshape(shape)
+                        for a in (w.rho, w.u, w.v, w.w, w.p))
+    if np.any(rho <= 0.0) or np.any(p <= 0.0):
+        raise AdmissibilityError("initial field is inadmissible")
+    e = p / (gas.gamma - 1.0) + 0.5 * rho * (u * u + v * v + ww * ww)
+    q = np.stack([rho, rho * u, rho * v, rho * ww, e], axis=-1)  # (n, nqv, 5)
+    ref = np.einsum("iq,nqv->nvi", t.projector, q)  # (n, 5, nb) reference basis
+    disc = _get_disc(mesh, geo, gas, BoundaryConditions(Conserved(1.0, 0.0, 0.0, 0.0, 1.0)))
+    rows = disc.new_state()
+    rows[:, : N_VARS * t.nb] = torch.from_numpy(ref.reshape(mesh.n_cells, -1)).to(disc.device)
+    return DofState(disc.from_reference(rows).clone())
+
+
+def face_flux_pass(state: DofState, aux, mesh: TetMesh, geo: DeviceGeometry, bcs: BoundaryConditions,
+                   gas: GasModel) -> FaceFluxBuffer:
+    """Interface fluxes at every face quadrature point (hodg/dg.py:594-621)."""
+    if aux is not None:
+        raise NotImplementedError("viscous auxiliary gradients are not in the B200 path")
+    disc = _get_disc(mesh, geo, gas, bcs)
+    prec = _prec_of(state)
+    rows = disc.to_reference(state.coeffs)
+    disc.reset_errors()
+    hbuf = disc.face_flux(rows, prec, hbuf=_torch().empty_like(disc.face_buffer(prec)))
+    disc.raise_errors(state.iteration)
+    return FaceFluxBuffer(inviscid=hbuf.transpose(1, 2))
+
+
+def accumulate_rhs(state: DofState, aux, fluxes: FaceFluxBuffer, mesh: TetMesh, geo: DeviceGeometry,
+                   bcs: BoundaryConditions, gas: GasModel) -> Residual:
+    """Volume terms plus the gather of stored face fluxes (hodg/dg.py:624-649)."""
+    torch = _torch()
+    disc = _get_disc(mesh, geo, gas, bcs)
+    prec = _prec_of(state)
+    rows = disc.to_reference(state.coeffs)
+    dt = torch.float32 if prec == _lib.PREC_MIXED else torch.float64
+    hbuf = torch.as_tensor(fluxes.inviscid, device=disc.device).to(dt).transpose(1, 2).contiguous()
+    disc.reset_errors()
+    res = disc.residual_rows(rows, hbuf, prec)
+    disc.raise_errors(state.iteration)
+    return Residual(res=disc.from_reference(res))
+
+
+def rhs(state: DofState, mesh: TetMesh, geo: DeviceGeometry, bcs: BoundaryConditions, gas: GasModel) -> Residual:
+    """Full spatial residual: face-flux pass then element accumulation
+    (hodg/dg.py:652-663)."""
+    disc = _get_disc(mesh, geo, gas, bcs)
+    prec = _prec_of(state)
+    rows = disc.to_reference(state.coeffs)
+    disc.reset_errors()
+    hbuf = disc.face_flux(rows, prec)
+    res = disc.residual_rows(rows, hbuf, prec)
+    disc.raise_errors(state.iteration)
+    return Residual(res=disc.from_reference(res))
+
+
+def cell_means(state: DofState, geo: DeviceGeometry):
+    """Cell-average conserved state (n_cells, 5) float64 (hodg/dg.py:666-668):
+    the mean of the reference-basis expansion."""
+    disc = next(iter(geo._disc_cache.values()), None)
+    if disc is None:
+        raise RuntimeError("no discretization bound to this geometry yet")
+    rows = disc.to_reference(state.coeffs)
+    t = ref_tables(geo.order)
+    mean = _torch().from_numpy(t.MEAN).to(disc.device)
+    return rows[:, : N_VARS * t.nb].reshape(disc.n, N_VARS, t.nb) @ mean

@@ -1,0 +1,110 @@
+"""Compact per-element / per-face geometry for the device kernels.
+
+Replaces the reference's per-cell x per-quadrature-point tables
+(`hodg/geometry.py:33-220`; about 8 GB at one million P2 tetrahedra) by
+16 doubles per element and 4 per face:
+
+  egeo  (N, 16): J^-1 (row-major, 9), fc[s] = sgn_s * area_s / vol (4), h, vol, 0
+  econv (N, 18): A = J / h and A^-1 (modal transforms to/from the Taylor basis)
+  efaces (N, 4): face id of local face s
+  fcells (F, 2), finfo (F,) = slotL | slotR << 2 | bc << 4, fnrm (F, 4)
+
+with J = [V1 - V0, V2 - V0, V3 - V0] (vertices ascending) the affine map of
+the reference tetrahedron.  Everything else is a compile-time constant of
+the order (refelem.py).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .mesh import TetMesh
+from .refelem import ref_tables
+
+__all__ = ["GeometryError", "DeviceGeometry", "compute_geometry", "volume_points"]
+
+
+class GeometryError(Exception):
+    pass
+
+
+@dataclass
+class DeviceGeometry:
+    order: int
+    n_basis: int
+    egeo: np.ndarray
+    econv: np.ndarray
+    efaces: np.ndarray
+    fcells: np.ndarray
+    finfo: np.ndarray
+    fnrm: np.ndarray
+    _dev: dict = field(default_factory=dict, repr=False)
+    _disc_cache: dict = field(default_factory=dict, repr=False)
+
+    @property
+    def n_vol_points(self) -> int:
+        return ref_tables(self.order).nqv
+
+    @property
+    def n_face_points(self) -> int:
+        return ref_tables(self.order).nqf
+
+    def device(self, device="cuda"):
+        """Device copies (torch tensors), uploaded once per device."""
+        import torch
+
+        d = self._dev.get(str(device))
+        if d is None:
+            d = {k: torch.from_numpy(np.ascontiguousarray(getattr(self, k))).to(device)
+                 for k in ("egeo", "econv", "efaces", "fcells", "finfo", "fnrm")}
+            self._dev[str(device)] = d
+        return d
+
+    def constant_count(self) -> int:
+        return sum(getattr(self, k).size for k in ("egeo", "econv", "fnrm"))
+
+
+def element_jacobians(mesh: TetMesh):
+    V = mesh.node_xy[mesh.cell_nodes.astype(np.int64)]
+    J = np.stack([V[:, 1] - V[:, 0], V[:, 2] - V[:, 0], V[:, 3] - V[:, 0]], axis=2)  # J[:, d, k]
+    return V, J
+
+
+def compute_geometry(mesh: TetMesh, order: int) -> DeviceGeometry:
+    if order not in (0, 1, 2, 3):
+        raise GeometryError(f"unsupported order {order}; expected 0..3")
+    codes = mesh.boundary_kind_codes()
+    if np.any(codes < 0):
+        raise GeometryError(f"boundary face {int(np.flatnonzero(codes < 0)[0])} has no boundary patch")
+    n = mesh.n_cells
+    V, J = element_jacobians(mesh)
+    det = np.linalg.det(J)
+    if np.any(np.abs(det) <= 0.0):
+        raise GeometryError("degenerate element")
+    Jinv = np.linalg.inv(J)
+    vol = mesh.cell_area
+    h = mesh.cell_h
+    fc = mesh.cell_fsign * mesh.face_length[mesh.cell_faces] / vol[:, None]
+    egeo = np.zeros((n, 16))
+    egeo[:, 0:9] = Jinv.reshape(n, 9)
+    egeo[:, 9:13] = fc
+    egeo[:, 13] = h
+    egeo[:, 14] = vol
+    econv = np.empty((n, 18))
+    econv[:, 0:9] = (J / h[:, None, None]).reshape(n, 9)
+    econv[:, 9:18] = (Jinv * h[:, None, None]).reshape(n, 9)
+    slots = mesh.face_slots.astype(np.int32)
+    finfo = (slots[:, 0] | (np.maximum(slots[:, 1], 0) << 2) | (codes.astype(np.int32) << 4)).astype(np.int32)
+    fnrm = np.zeros((mesh.n_faces, 4))
+    fnrm[:, :3] = mesh.face_normal
+    return DeviceGeometry(order, ref_tables(order).nb, egeo, econv, mesh.cell_faces.astype(np.int32),
+                          mesh.face_cells.astype(np.int32), finfo, fnrm)
+
+
+def volume_points(mesh: TetMesh, order: int) -> np.ndarray:
+    """(N, nqv, 3) physical volume quadrature points, x = V0 + J xi."""
+    V, J = element_jacobians(mesh)
+    xi = ref_tables(order).vol_points[:, 1:4]
+    return V[:, None, 0, :] + np.einsum("ndk,qk->nqd", J, xi)

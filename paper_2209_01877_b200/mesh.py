@@ -1,0 +1,416 @@
+"""Unstructured tetrahedral meshes: flat arrays indexed by entity id, the 3D
+analogue of the reference's `hodg/mesh.py` (Mesh arrays :97-174, face
+discovery :241-286, generators :361-393, perturbation :396-425, HODG-MESH
+text format :431-560, validation :566-629).
+
+Conventions (the device kernels rely on them):
+  * each element's four node ids are stored ascending; local face s is the
+    face opposite local vertex s, its vertices in ascending order -- so the
+    two elements sharing a face enumerate its vertices (and, the face rules
+    being fully symmetric, its quadrature points) identically;
+  * face ids follow the first traversal over (element, slot), the first
+    traverser is the left element, the unit normal points left -> right
+    (outward at boundaries), as in the reference's 2D builder;
+  * `cell_area` holds element volumes and `face_length` face areas, keeping
+    the reference's field names.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+__all__ = [
+    "BC_KINDS",
+    "MeshError",
+    "MeshParseError",
+    "TopologyError",
+    "BoundaryPatch",
+    "TetMesh",
+    "build_tet_mesh",
+    "generate_tet_box",
+    "perturb_interior_nodes",
+    "save_mesh",
+    "load_mesh",
+    "validate",
+]
+
+BC_KINDS = ("far_field", "slip_wall", "no_slip_wall")
+FACE_LOCAL = np.array([[1, 2, 3], [0, 2, 3], [0, 1, 3], [0, 1, 2]], dtype=np.int64)
+
+
+class MeshError(Exception):
+    pass
+
+
+class MeshParseError(MeshError):
+    def __init__(self, path, line_no, message):
+        super().__init__(f"{path}:{line_no}: {message}")
+        self.line_no = line_no
+
+
+class TopologyError(MeshError):
+    pass
+
+
+@dataclass(frozen=True)
+class BoundaryPatch:
+    name: str
+    kind: str
+    face_ids: np.ndarray
+
+    def __post_init__(self):
+        if self.kind not in BC_KINDS:
+            raise MeshError(f"unknown boundary kind {self.kind!r}")
+
+
+@dataclass
+class TetMesh:
+    node_xy: np.ndarray  # (n_nodes, 3)
+    cell_nodes: np.ndarray  # (N, 4) int32 ascending
+    cell_faces: np.ndarray  # (N, 4) int32, slot s = face opposite vertex s
+    cell_fsign: np.ndarray  # (N, 4) int8: +1 left, -1 right
+    cell_neighbors: np.ndarray  # (N, 4) int32, -1 at boundary
+    cell_centroid: np.ndarray  # (N, 3)
+    cell_area: np.ndarray  # (N,) volume
+    cell_h: np.ndarray  # (N,) cbrt(volume)
+    face_nodes: np.ndarray  # (F, 3) int32 ascending
+    face_cells: np.ndarray  # (F, 2) int32, right = -1 at boundary
+    face_slots: np.ndarray  # (F, 2) int8, local slot in left / right element (-1)
+    face_normal: np.ndarray  # (F, 3) unit, left -> right
+    face_length: np.ndarray  # (F,) area
+    face_patch: np.ndarray  # (F,) int32 patch index or -1
+    patches: list = field(default_factory=list)
+
+    dim = 3
+
+    @property
+    def n_nodes(self) -> int:
+        return self.node_xy.shape[0]
+
+    @property
+    def n_cells(self) -> int:
+        return self.cell_nodes.shape[0]
+
+    @property
+    def n_faces(self) -> int:
+        return self.face_nodes.shape[0]
+
+    @property
+    def n_interior_faces(self) -> int:
+        return int(np.count_nonzero(self.face_cells[:, 1] >= 0))
+
+    @property
+    def cell_nvert(self) -> np.ndarray:
+        return np.full(self.n_cells, 4, dtype=np.int8)
+
+    def boundary_kind_codes(self) -> np.ndarray:
+        """0 interior, 1 far_field, 2 slip_wall, 3 no_slip_wall, -1 unpatched
+        boundary (hodg/mesh.py:166-174)."""
+        codes = np.zeros(self.n_faces, dtype=np.int8)
+        codes[self.face_cells[:, 1] < 0] = -1
+        for p, patch in enumerate(self.patches):
+            codes[self.face_patch == p] = BC_KINDS.index(patch.kind) + 1
+        return codes
+
+    def raw(self):
+        """(nodes, elements, patch specs) that rebuild this mesh."""
+        specs = [(p.name, p.kind, [tuple(int(x) for x in self.face_nodes[f]) for f in p.face_ids])
+                 for p in self.patches]
+        return self.node_xy, self.cell_nodes, specs
+
+
+def _signed_volume6(V):
+    a = V[:, 1] - V[:, 0]
+    b = V[:, 2] - V[:, 0]
+    c = V[:, 3] - V[:, 0]
+    return np.einsum("nd,nd->n", a, np.cross(b, c))
+
+
+def build_tet_mesh(node_xyz, tets, patch_specs=None) -> TetMesh:
+    """Assemble a tetrahedral mesh from nodes, element->node lists and
+    boundary patches [(name, kind, [(a, b, c), ...]), ...]."""
+    X = np.ascontiguousarray(node_xyz, dtype=np.float64)
+    if X.ndim != 2 or X.shape[1] != 3:
+        raise MeshError("node coordinates must be an (n, 3) array")
+    if not np.all(np.isfinite(X)):
+        raise TopologyError("non-finite node coordinates")
+    T = np.asarray(tets, dtype=np.int64)
+    if T.ndim != 2 or T.shape[1] != 4 or T.shape[0] == 0:
+        raise MeshError("elements must be a non-empty (N, 4) array")
+    if T.min() < 0 or T.max() >= X.shape[0]:
+        raise TopologyError("element node index out of range")
+    T = np.sort(T, axis=1)
+    if np.any(T[:, 1:] == T[:, :-1]):
+        raise TopologyError("element with a repeated node")
+    n = T.shape[0]
+    V = X[T]
+    vol = np.abs(_signed_volume6(V)) / 6.0
+    if np.any(vol <= 0.0):
+        raise TopologyError(f"element {int(np.argmin(vol))}: degenerate (zero volume)")
+    centroid = 0.25 * (V[:, 0] + V[:, 1] + V[:, 2] + V[:, 3])
+    h = np.cbrt(vol)
+
+    # face discovery: pack the ascending triple into one 64-bit key
+    nn = np.int64(X.shape[0])
+    tri = T[:, FACE_LOCAL].reshape(-1, 3)  # (4n, 3), slot-major within element
+    key = (tri[:, 0] * nn + tri[:, 1]) * nn + tri[:, 2]
+    order = np.argsort(key, kind="stable")  # ties keep traversal order
+    ks = key[order]
+    new_run = np.empty(ks.size, dtype=bool)
+    new_run[0] = True
+    new_run[1:] = ks[1:] != ks[:-1]
+    run_id = np.cumsum(new_run) - 1
+    run_start = np.flatnonzero(new_run)
+    run_len = np.diff(np.append(run_start, ks.size))
+    if run_len.max() > 2:
+        raise TopologyError("face shared by more than two elements (non-manifold)")
+    first_slot = order[run_start]  # first traversal of each distinct face
+    face_rank = np.empty(run_start.size, dtype=np.int64)
+    face_rank[np.argsort(first_slot, kind="stable")] = np.arange(run_start.size)
+    slot_face = np.empty(4 * n, dtype=np.int64)
+    slot_face[order] = face_rank[run_id]
+    F = run_start.size
+    left_slot = np.empty(F, dtype=np.int64)
+    left_slot[face_rank] = first_slot
+    right_slot = np.full(F, -1, dtype=np.int64)
+    two = run_len == 2
+    right_slot[face_rank[two]] = order[run_start[two] + 1]
+
+    face_cells = np.stack([left_slot // 4, np.where(right_slot >= 0, right_slot // 4, -1)], axis=1).astype(np.int32)
+    face_slots = np.stack([left_slot % 4, np.where(right_slot >= 0, right_slot % 4, -1)], axis=1).astype(np.int8)
+    face_nodes = tri[left_slot].astype(np.int32)
+    cell_faces = slot_face.reshape(n, 4).astype(np.int32)
+    sign = np.full(4 * n, -1, dtype=np.int8)
+    sign[left_slot] = 1
+    cell_fsign = sign.reshape(n, 4)
+
+    A = X[face_nodes[:, 0]]
+    cr = np.cross(X[face_nodes[:, 1]] - A, X[face_nodes[:, 2]] - A)
+    norm = np.sqrt(np.einsum("fd,fd->f", cr, cr))
+    if np.any(norm <= 0.0):
+        raise TopologyError("zero-area face")
+    normal = cr / norm[:, None]
+    opp = X[T[face_cells[:, 0], face_slots[:, 0]]]  # left element's vertex opposite the face
+    inward = np.einsum("fd,fd->f", normal, A - opp) < 0.0
+    normal[inward] = -normal[inward]
+    area = 0.5 * norm
+
+    fc = face_cells[cell_faces]
+    cell_neighbors = np.where(fc[..., 0] == np.arange(n)[:, None], fc[..., 1], fc[..., 0]).astype(np.int32)
+
+    face_patch = np.full(F, -1, dtype=np.int32)
+    patches = []
+    if patch_specs:
+        fkey = (face_nodes[:, 0].astype(np.int64) * nn + face_nodes[:, 1]) * nn + face_nodes[:, 2]
+        srt = np.argsort(fkey)
+        for p, (name, kind, tris) in enumerate(patch_specs):
+            t3 = np.sort(np.asarray(tris, dtype=np.int64).reshape(-1, 3), axis=1)
+            k = (t3[:, 0] * nn + t3[:, 1]) * nn + t3[:, 2]
+            pos = np.searchsorted(fkey[srt], k)
+            ok = (pos < F) & (fkey[srt][np.minimum(pos, F - 1)] == k)
+            if not np.all(ok):
+                raise TopologyError(f"patch {name!r}: no face with nodes {t3[~ok][0].tolist()}")
+            ids = srt[pos]
+            if np.any(face_cells[ids, 1] >= 0):
+                raise TopologyError(f"patch {name!r}: interior face")
+            if np.any(face_patch[ids] != -1):
+                raise TopologyError(f"patch {name!r}: face already in another patch")
+            face_patch[ids] = p
+            patches.append(BoundaryPatch(name, kind, np.sort(ids).astype(np.int32)))
+
+    return TetMesh(X, T.astype(np.int32), cell_faces, cell_fsign, cell_neighbors, centroid, vol, h,
+                   face_nodes, face_cells, face_slots, normal, area, face_patch, patches)
+
+
+# six monotone lattice paths 000 -> 111 (Kuhn / Freudenthal split)
+_PATHS = ((0, 1, 2), (0, 2, 1), (1, 0, 2), (1, 2, 0), (2, 0, 1), (2, 1, 0))
+_SIDES = ("xmin", "xmax", "ymin", "ymax", "zmin", "zmax")
+
+
+def generate_tet_box(nx: int, ny: int | None = None, nz: int | None = None,
+                     extent=(0.0, 0.0, 0.0, 1.0, 1.0, 1.0), bc="far_field") -> TetMesh:
+    """Structured hexahedral lattice, each hex split into six tetrahedra
+    along its main diagonal (conforming; 6 nx ny nz elements).  `bc` is one
+    kind or a dict keyed by xmin..zmax.  Elements are numbered hex-major
+    (x fastest), path-minor."""
+    ny = nx if ny is None else ny
+    nz = nx if nz is None else nz
+    if min(nx, ny, nz) < 1:
+        raise MeshError("box dimensions must be at least 1")
+    x0, y0, z0, x1, y1, z1 = extent
+    gx, gy, gz = np.linspace(x0, x1, nx + 1), np.linspace(y0, y1, ny + 1), np.linspace(z0, z1, nz + 1)
+    nodes = np.stack(np.meshgrid(gx, gy, gz, indexing="ij"), axis=-1).transpose(2, 1, 0, 3).reshape(-1, 3)
+
+    def nid(i, j, k):
+        return (k * (ny + 1) + j) * (nx + 1) + i
+
+    k3, j3, i3 = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+    i3, j3, k3 = i3.ravel(), j3.ravel(), k3.ravel()
+    elems = np.empty((i3.size, 6, 4), dtype=np.int64)
+    for p, path in enumerate(_PATHS):
+        off = np.zeros(3, dtype=np.int64)
+        elems[:, p, 0] = nid(i3, j3, k3)
+        for s, ax in enumerate(path):
+            off[ax] += 1
+            elems[:, p, s + 1] = nid(i3 + off[0], j3 + off[1], k3 + off[2])
+    kinds = {s: bc for s in _SIDES} if isinstance(bc, str) else dict(bc)
+    specs = []
+    for side in _SIDES:
+        axis = "xyz".index(side[0])
+        fixed = 0 if side.endswith("min") else (nx, ny, nz)[axis]
+        u_ax, w_ax = [a for a in range(3) if a != axis]
+        nu, nw = (nx, ny, nz)[u_ax], (nx, ny, nz)[w_ax]
+        uu, ww = np.meshgrid(np.arange(nu), np.arange(nw), indexing="ij")
+        uu, ww = uu.ravel(), ww.ravel()
+
+        def corner(du, dw):
+            idx = [None, None, None]
+            idx[axis] = np.full(uu.size, fixed)
+            idx[u_ax] = uu + du
+            idx[w_ax] = ww + dw
+            return nid(*idx)
+
+        lo, hi = corner(0, 0), corner(1, 1)
+        tris = np.concatenate([np.stack([lo, corner(1, 0), hi], axis=1), np.stack([lo, corner(0, 1), hi], axis=1)])
+        specs.append((side, kinds[side], tris))
+    return build_tet_mesh(nodes, elems.reshape(-1, 4), specs)
+
+
+def perturb_interior_nodes(mesh: TetMesh, amplitude: float, seed: int = 0) -> TetMesh:
+    """Interior nodes moved by amplitude x (shortest incident edge) x
+    U(-1, 1)^3; boundary nodes fixed, patches preserved (3D analogue of
+    hodg/mesh.py:396-425)."""
+    rng = np.random.default_rng(seed)
+    X = mesh.node_xy
+    T = mesh.cell_nodes.astype(np.int64)
+    e = T[:, [[0, 1], [0, 2], [0, 3], [1, 2], [1, 3], [2, 3]]].reshape(-1, 2)
+    length = np.linalg.norm(X[e[:, 0]] - X[e[:, 1]], axis=1)
+    shortest = np.full(mesh.n_nodes, np.inf)
+    np.minimum.at(shortest, e[:, 0], length)
+    np.minimum.at(shortest, e[:, 1], length)
+    offsets = rng.uniform(-1.0, 1.0, size=X.shape)
+    movable = np.ones(mesh.n_nodes, dtype=bool)
+    movable[np.unique(mesh.face_nodes[mesh.face_cells[:, 1] < 0])] = False
+    Y = X.copy()
+    Y[movable] += amplitude * shortest[movable, None] * offsets[movable]
+    nodes, elems, specs = mesh.raw()
+    return build_tet_mesh(Y, elems, specs)
+
+
+def save_mesh(mesh: TetMesh, path) -> None:
+    """HODG-MESH v1 with a `dim 3` line: `x y z` nodes, `T a b c d`
+    elements, patch faces as node triples (hodg/mesh.py:431-447)."""
+    with open(path, "w") as fh:
+        fh.write("hodg-mesh 1\ndim 3\n")
+        fh.write(f"nodes {mesh.n_nodes}\n")
+        for x, y, z in mesh.node_xy:
+            fh.write(f"{float(x)!r} {float(y)!r} {float(z)!r}\n")
+        fh.write(f"cells {mesh.n_cells}\n")
+        for t in mesh.cell_nodes:
+            fh.write("T " + " ".join(str(int(v)) for v in t) + "\n")
+        fh.write(f"patches {len(mesh.patches)}\n")
+        for p in mesh.patches:
+            fh.write(f"{p.name} {p.kind} {len(p.face_ids)}\n")
+            for f in p.face_ids:
+                fh.write(" ".join(str(int(v)) for v in mesh.face_nodes[f]) + "\n")
+
+
+def load_mesh(path) -> TetMesh:
+    """Read a 3D HODG-MESH file; MeshParseError carries the line number
+    (hodg/mesh.py:450-560)."""
+    with open(path) as fh:
+        raw = fh.read().splitlines()
+    lines = [(i + 1, s.strip()) for i, s in enumerate(raw) if s.strip() and not s.strip().startswith("#")]
+    it = iter(lines)
+
+    def nxt(what):
+        try:
+            return next(it)
+        except StopIteration:
+            raise MeshParseError(path, len(raw), f"expected {what}") from None
+
+    ln, s = nxt("header")
+    if s.split() != ["hodg-mesh", "1"]:
+        raise MeshParseError(path, ln, "expected header 'hodg-mesh 1'")
+    ln, s = nxt("'dim 3'")
+    if s.split() != ["dim", "3"]:
+        raise MeshParseError(path, ln, "expected 'dim 3'")
+
+    def count(word):
+        ln, s = nxt(f"'{word} N'")
+        parts = s.split()
+        if len(parts) != 2 or parts[0] != word:
+            raise MeshParseError(path, ln, f"expected '{word} N'")
+        try:
+            return int(parts[1])
+        except ValueError:
+            raise MeshParseError(path, ln, f"bad {word} count") from None
+
+    nn = count("nodes")
+    X = np.empty((nn, 3))
+    for i in range(nn):
+        ln, s = nxt("node line")
+        parts = s.split()
+        try:
+            if len(parts) != 3:
+                raise ValueError
+            X[i] = [float(v) for v in parts]
+        except ValueError:
+            raise MeshParseError(path, ln, "expected 'x y z'") from None
+    ne = count("cells")
+    T = np.empty((ne, 4), dtype=np.int64)
+    for i in range(ne):
+        ln, s = nxt("cell line")
+        parts = s.split()
+        if len(parts) != 5 or parts[0] != "T":
+            raise MeshParseError(path, ln, "expected 'T a b c d'")
+        try:
+            T[i] = [int(v) for v in parts[1:]]
+        except ValueError:
+            raise MeshParseError(path, ln, "bad node index") from None
+    specs = []
+    np_ = count("patches")
+    for _ in range(np_):
+        ln, s = nxt("'name kind count'")
+        parts = s.split()
+        if len(parts) != 3 or parts[1] not in BC_KINDS:
+            raise MeshParseError(path, ln, "expected 'name kind count' with a known kind")
+        tris = []
+        for _ in range(int(parts[2])):
+            ln2, s2 = nxt("'a b c'")
+            try:
+                tris.append(tuple(int(v) for v in s2.split()))
+                if len(tris[-1]) != 3:
+                    raise ValueError
+            except ValueError:
+                raise MeshParseError(path, ln2, "expected 'a b c'") from None
+        specs.append((parts[0], parts[1], tris))
+    mesh = build_tet_mesh(X, T, specs)
+    problems = validate(mesh)
+    if problems:
+        raise TopologyError(f"{path}: " + "; ".join(problems[:5]))
+    return mesh
+
+
+def validate(mesh: TetMesh) -> list[str]:
+    """Invariant checks; violations are returned, not raised
+    (hodg/mesh.py:566-629): geometric closure sum(sgn n A) = 0 per element,
+    unit normals, face <-> element back references, patch coverage."""
+    problems = []
+    n_vec = mesh.face_normal[mesh.cell_faces] * (mesh.face_length[mesh.cell_faces] *
+                                                  mesh.cell_fsign)[..., None]
+    closure = np.linalg.norm(n_vec.sum(axis=1), axis=1)
+    scale = mesh.face_length[mesh.cell_faces].sum(axis=1)
+    bad = np.flatnonzero(closure > 1e-12 * scale)
+    problems += [f"cell {c}: geometric closure violated" for c in bad[:5]]
+    nrm = np.linalg.norm(mesh.face_normal, axis=1)
+    problems += [f"face {f}: normal not unit length" for f in np.flatnonzero(np.abs(nrm - 1.0) > 1e-14)[:5]]
+    fc = mesh.face_cells[mesh.cell_faces]
+    me = np.arange(mesh.n_cells)[:, None]
+    ok = (fc[..., 0] == me) | (fc[..., 1] == me)
+    problems += [f"cell {c}: face does not reference it back" for c in np.flatnonzero(~ok.all(axis=1))[:5]]
+    unpatched = (mesh.face_cells[:, 1] < 0) & (mesh.face_patch < 0)
+    problems += [f"face {f}: boundary face without a patch" for f in np.flatnonzero(unpatched)[:5]]
+    return problems

@@ -1,0 +1,184 @@
+"""CUDA residual path vs the CPU oracle (which is pinned to the reference's
+golden files).  North-star tolerances: FP64 relative L2 <= 1e-12, mixed
+precision <= 1e-5."""
+
+import numpy as np
+import pytest
+
+from gpu_helpers import meshes, oracle_state, rel, to_oracle
+from oracle import solver as S
+
+pytestmark = pytest.mark.gpu
+
+FP64_TOL = 1e-12
+MIXED_TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2209_01877_b200 as P
+
+    P._lib.lib()  # fail loudly if the CUDA library / device is missing
+    return P
+
+
+def gpu_setup(P, m, order, mach=0.4, angle=10.0, flux="roe"):
+    gas = P.GasModel()
+    geo = P.compute_geometry(m, order)
+    bcs = P.BoundaryConditions(P.freestream_conserved(gas, mach, angle), flux)
+    return gas, geo, bcs
+
+
+@pytest.mark.parametrize("order", [0, 1, 2, 3])
+@pytest.mark.parametrize("flux,kind", [("roe", 0), ("llf", 1)])
+def test_rhs_fp64_matches_oracle(P, order, flux, kind):
+    import torch
+
+    for name, m in meshes():
+        disc, c = oracle_state(m, order, flux_kind=kind)
+        gas, geo, bcs = gpu_setup(P, m, order, flux=flux)
+        r = P.rhs(P.DofState(torch.from_numpy(c).cuda()), m, geo, bcs, gas).res.cpu().numpy()
+        ref = disc.rhs(c)
+        assert rel(r, ref) <= FP64_TOL, (name, order, flux, rel(r, ref))
+
+
+@pytest.mark.parametrize("order", [1, 2, 3])
+def test_face_flux_fp64_matches_oracle(P, order):
+    import torch
+
+    for name, m in meshes():
+        disc, c = oracle_state(m, order)
+        gas, geo, bcs = gpu_setup(P, m, order)
+        buf = P.face_flux_pass(P.DofState(torch.from_numpy(c).cuda()), None, m, geo, bcs, gas)
+        f = buf.inviscid.cpu().numpy()
+        ref = disc.flux_pass(c)
+        assert f.shape == ref.shape
+        assert rel(f, ref) <= FP64_TOL, (name, order, rel(f, ref))
+        # accumulate_rhs on the oracle's own face buffer
+        res = P.accumulate_rhs(P.DofState(torch.from_numpy(c).cuda()), None,
+                               P.FaceFluxBuffer(torch.from_numpy(ref).cuda()), m, geo, bcs, gas)
+        assert rel(res.res.cpu().numpy(), disc.rhs_pass(c, ref)) <= FP64_TOL
+
+
+@pytest.mark.parametrize("order", [1, 2, 3])
+def test_rhs_mixed_matches_oracle(P, order):
+    import torch
+
+    for name, m in meshes():
+        disc, c = oracle_state(m, order)
+        gas, geo, bcs = gpu_setup(P, m, order)
+        st = P.DofState(torch.from_numpy(c).cuda().to(torch.float32))
+        r = P.rhs(st, m, geo, bcs, gas).res.cpu().numpy()
+        ref = disc.rhs(c)  # FP64 oracle of the same (rounded) state
+        ref32 = disc.rhs(np.ascontiguousarray(c.astype(np.float32)))  # reference MP semantics
+        assert rel(r, ref) <= MIXED_TOL, (name, order, rel(r, ref))
+        assert rel(r, ref32) <= MIXED_TOL, (name, order, rel(r, ref32))
+
+
+@pytest.mark.parametrize("order", [0, 1, 2, 3])
+def test_freestream_preserved(P, order):
+    import torch
+
+    for name, m in meshes():
+        gas, geo, bcs = gpu_setup(P, m, order, mach=0.3)
+        w = P.freestream_primitive(gas, 0.3, 10.0)
+        st = P.project_initial(m, geo, lambda x, y, z: w, gas)
+        r = P.rhs(st, m, geo, bcs, gas).res
+        scale = 1e-11 * (10.0 ** order)
+        assert float(r.abs().max()) < scale, (name, order, float(r.abs().max()))
+
+
+def test_projection_matches_oracle(P):
+    for order in (1, 2, 3):
+        for name, m in meshes():
+            disc, _ = oracle_state(m, order)
+            gas, geo, bcs = gpu_setup(P, m, order)
+            f = lambda x, y, z: P.vortex_primitive(gas, 0.4, 10.0, 2.0, 1.0, 0.5, 0.0, x, y)  # noqa: E731
+            c = P.project_initial(m, geo, f, gas).coeffs.cpu().numpy()
+            om = disc.mesh
+            ref = S.project_initial(om, disc.tab, lambda x, y, z: S.vortex_primitive(
+                S.Gas(), 0.4, 10.0, 2.0, 1.0, 0.5, 0.0, x, y, dim=3), S.Gas())
+            assert rel(c, ref) <= 1e-13, (name, order, rel(c, ref))
+
+
+def test_local_dt_and_min_reduce(P):
+    import torch
+
+    for order in (1, 2):
+        for name, m in meshes():
+            disc, c = oracle_state(m, order)
+            gas, geo, bcs = gpu_setup(P, m, order)
+            dt = P.local_dt_field(P.DofState(torch.from_numpy(c).cuda()), m, geo, gas, 0.3, order, bcs)
+            ref = S.local_dt_field(disc, c, 0.3, order)
+            assert rel(dt.cpu().numpy(), ref) <= 1e-13
+            assert P.min_reduce(dt) == float(np.min(dt.cpu().numpy()))
+
+
+@pytest.mark.parametrize("scheme", ["rk2", "rk3"])
+@pytest.mark.parametrize("dt_mode", ["global", "local"])
+def test_run_history_matches_oracle(P, scheme, dt_mode):
+    """10 steps of the fused stepper vs the oracle's RK loop: residual
+    history and final state within 1e-12 (BASELINE config 1 shape)."""
+    m = P.perturb_interior_nodes(P.generate_tet_box(4, extent=(0.0, 0.0, 0.0, 10.0, 10.0, 2.5),
+                                                    bc={"xmin": "far_field", "xmax": "far_field",
+                                                        "ymin": "far_field", "ymax": "far_field",
+                                                        "zmin": "slip_wall", "zmax": "slip_wall"}), 0.1, 3)
+    cfg = P.RunConfig(order=1, mach=0.5, initial_kind="vortex", initial_x0=5.0, initial_y0=5.0, cfl=0.3,
+                      dt_mode=dt_mode, scheme=scheme, max_iterations=10, log_every=1)
+    art = P.run(cfg, mesh=m)
+    spec = S.RunSpec(mesh=to_oracle(m), order=1, mach=0.5, initial="vortex", x0=5.0, y0=5.0, cfl=0.3,
+                     dt_mode=dt_mode, scheme=scheme, max_iterations=10, log_every=1)
+    u, hist, _ = S.run(spec)
+    assert rel(art.final_state.coeffs.cpu().numpy(), u) <= FP64_TOL
+    assert rel(np.array(art.history.res), np.array(hist.res)) <= FP64_TOL
+    assert rel(np.array(art.history.dts), np.array(hist.dts)) <= FP64_TOL
+
+
+def test_rk_functional_api_matches_fused(P):
+    import torch
+
+    m = P.generate_tet_box(3)
+    gas, geo, bcs = gpu_setup(P, m, 2)
+    disc, c = oracle_state(m, 2)
+    st = P.DofState(torch.from_numpy(c).cuda())
+    dt = P.min_reduce(P.local_dt_field(st, m, geo, gas, 0.3, 2, bcs))
+    calls = []
+
+    def fn(s):
+        calls.append(1)
+        return P.rhs(s, m, geo, bcs, gas)
+
+    out = P.rk3_step(st, dt, fn)
+    assert len(calls) == 3
+    ref = S.rk3_step(c, dt, lambda x: disc.rhs(x))
+    assert rel(out.coeffs.cpu().numpy(), ref) <= FP64_TOL
+    out2 = P.rk2_step(st, dt, fn)
+    ref2 = S.rk2_step(c, dt, lambda x: disc.rhs(x))
+    assert rel(out2.coeffs.cpu().numpy(), ref2) <= FP64_TOL
+
+
+def test_admissibility_error_carries_cell_and_iteration(P):
+    import torch
+
+    m = P.generate_tet_box(3)
+    gas, geo, bcs = gpu_setup(P, m, 1)
+    w = P.freestream_primitive(gas, 0.3, 10.0)
+    st = P.project_initial(m, geo, lambda x, y, z: w, gas)
+    st.coeffs[4, 0, 0] = -1.0
+    st.iteration = 17
+    with pytest.raises(P.AdmissibilityError) as err:
+        P.rhs(st, m, geo, bcs, gas)
+    assert "17" in str(err.value)
+    assert err.value.face is not None or err.value.cell == 4
+
+
+def test_deterministic_bitwise(P):
+    import torch
+
+    m = P.perturb_interior_nodes(P.generate_tet_box(5), 0.1, 2)
+    gas, geo, bcs = gpu_setup(P, m, 2)
+    _, c = oracle_state(m, 2)
+    st = P.DofState(torch.from_numpy(c).cuda())
+    r1 = P.rhs(st, m, geo, bcs, gas).res.clone()
+    r2 = P.rhs(st, m, geo, bcs, gas).res
+    assert torch.equal(r1, r2)
