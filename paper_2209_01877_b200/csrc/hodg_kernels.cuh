@@ -7,6 +7,8 @@
 // tables (hodg/geometry.py:33-51) collapse into compile-time constants and
 // the per-element data is 16 doubles (J^-1, sgn*area/vol per face, h, vol).
 
+#include <utility>
+
 #include "hodg_common.cuh"
 
 #define HODG_CAT_(a, b) a##b
@@ -28,6 +30,16 @@ constexpr int XS = 15;                        // smem slot per (element, qp): 5 
 
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 __host__ __device__ constexpr size_t cmax(size_t a, size_t b) { return a > b ? a : b; }
+
+// compile-time loop: f(std::integral_constant<int, I>) for I in [0, N)
+template <typename F, int... Is>
+__device__ __forceinline__ void sfor_impl(F&& f, std::integer_sequence<int, Is...>) {
+    (f(std::integral_constant<int, Is>{}), ...);
+}
+template <int N, typename F>
+__device__ __forceinline__ void sfor(F&& f) {
+    sfor_impl(f, std::make_integer_sequence<int, N>{});
+}
 
 // exponent d of monomial i in the graded order (degree, then descending x,
 // then descending y): the reference's `_EXPONENTS` order (hodg/basis.py:21) in 3D
@@ -228,13 +240,11 @@ __global__ void __launch_bounds__(ETHREADS) elem_stage_kernel(const hodg_mesh_de
         T c[NB];
 #pragma unroll
         for (int i = 0; i < NB; ++i) c[i] = T(S[e * RS + v * NB + i]);
-#pragma unroll
-        for (int q = 0; q < NQV; ++q) {
+        sfor<NQV>([&](auto q) {
             T u = T(0);
-#pragma unroll
-            for (int i = 0; i < NB; ++i) u += TAB(VB, T, q * NB + i) * c[i];
+            sfor<NB>([&](auto i) { u += TAB(VB, T, q * NB + i) * c[i]; });
             X[(q * E + e) * XS + v] = u;
-        }
+        });
     }
     __syncthreads();
 
@@ -276,21 +286,19 @@ __global__ void __launch_bounds__(ETHREADS) elem_stage_kernel(const hodg_mesh_de
         T acc[NB];
 #pragma unroll
         for (int i = 0; i < NB; ++i) acc[i] = T(0);
-#pragma unroll
-        for (int q = 0; q < NQV; ++q) {
+        sfor<NQV>([&](auto q) {
             const T* sl = X + (q * E + e) * XS;
             const T fd[3] = {sl[v], sl[5 + v], sl[10 + v]};
-#pragma unroll
-            for (int i = 0; i < NB; ++i)
-#pragma unroll
-                for (int d = 0; d < 3; ++d)
-                    if (expt(i, d) > 0) acc[i] += TAB(VD, T, (q * NB + i) * 3 + d) * fd[d];
-        }
+            sfor<NB>([&](auto i) {
+                sfor<3>([&](auto d) {
+                    if constexpr (expt(i, d) > 0) acc[i] += TAB(VD, T, (q * NB + i) * 3 + d) * fd[d];
+                });
+            });
+        });
         double accd[NB];
 #pragma unroll
         for (int i = 0; i < NB; ++i) accd[i] = double(acc[i]);
-#pragma unroll
-        for (int s = 0; s < 4; ++s) {
+        sfor<4>([&](auto s) {
             const int64_t f = FI[e * 4 + s];
             const T* H = hbuf + (f * 5 + v) * NQF;
             T hq[NQF];
@@ -299,22 +307,19 @@ __global__ void __launch_bounds__(ETHREADS) elem_stage_kernel(const hodg_mesh_de
             T fa[NB];
 #pragma unroll
             for (int i = 0; i < NB; ++i) fa[i] = T(0);
-#pragma unroll
-            for (int q = 0; q < NQF; ++q)
-#pragma unroll
-                for (int i = 0; i < NB; ++i) fa[i] += TAB(FG, T, (s * NQF + q) * NB + i) * hq[q];
+            sfor<NQF>([&](auto q) {
+                sfor<NB>([&](auto i) { fa[i] += TAB(FG, T, (s * NQF + q) * NB + i) * hq[q]; });
+            });
             const double fc = G[e * 16 + 9 + s];
 #pragma unroll
             for (int i = 0; i < NB; ++i) accd[i] -= fc * double(fa[i]);
-        }
+        });
         double r[NB];
-#pragma unroll
-        for (int j = 0; j < NB; ++j) {
+        sfor<NB>([&](auto j) {
             double z = 0.0;
-#pragma unroll
-            for (int k = 0; k < NB; ++k) z += MINV_T[j * NB + k] * accd[k];
+            sfor<NB>([&](auto k) { z += MINV_T[j * NB + k] * accd[k]; });
             r[j] = z;
-        }
+        });
         if (a.res) {
 #pragma unroll
             for (int j = 0; j < NB; ++j) a.res[gid * RS + v * NB + j] = r[j];
@@ -323,8 +328,7 @@ __global__ void __launch_bounds__(ETHREADS) elem_stage_kernel(const hodg_mesh_de
         if (a.combine >= 0) {
             const double dt = a.dt_is_vector ? a.dt[gid] : a.dt[0];
             double mean = 0.0;
-#pragma unroll
-            for (int j = 0; j < NB; ++j) {
+            sfor<NB>([&](auto j) {
                 const double us = S[e * RS + v * NB + j];
                 double o;
                 if (a.combine == 1) {
@@ -335,7 +339,7 @@ __global__ void __launch_bounds__(ETHREADS) elem_stage_kernel(const hodg_mesh_de
                 }
                 S[e * RS + v * NB + j] = o;
                 mean += MEAN_T[j] * o;
-            }
+            });
             RED[5 * E + v * E + e] = mean;
         }
     }
@@ -387,8 +391,7 @@ __global__ void local_dt_kernel(const hodg_mesh_desc m, const double* __restrict
 #pragma unroll
     for (int v = 0; v < 5; ++v) {
         double s = 0.0;
-#pragma unroll
-        for (int j = 0; j < NB; ++j) s += MEAN_T[j] * state[c * RS + v * NB + j];
+        sfor<NB>([&](auto j) { s += MEAN_T[j] * state[c * RS + v * NB + j]; });
         mm[v] = s;
     }
     double dt = 0.0;
@@ -413,7 +416,7 @@ __global__ void local_dt_kernel(const hodg_mesh_desc m, const double* __restrict
 // X = (x - xc)/h (hodg/basis.py), and the reference-element basis m_i(eta):
 // b_j(A eta) = sum_i T_ij m_i(eta), A = J/h.  to_reference: c' = T c with A;
 // back: c = T(A^-1) c'.  Each column is the product of |alpha_j| linear forms.
-__device__ __forceinline__ int mono_index(int a, int b, int c) {
+__host__ __device__ constexpr int mono_index(int a, int b, int c) {
     const int k = a + b + c;
     return k * (k + 1) * (k + 2) / 6 + (k - a) * (k - a + 1) / 2 + (k - a - b);
 }
@@ -430,42 +433,39 @@ __global__ void modal_transform_kernel(const hodg_mesh_desc m, int to_reference,
     for (int v = 0; v < 5; ++v)
 #pragma unroll
         for (int i = 0; i < NB; ++i) o[v][i] = 0.0;
-#pragma unroll
-    for (int j = 0; j < NB; ++j) {
+    sfor<NB>([&](auto j) {
+        // column j: product of |alpha_j| linear forms sum_m M[d][m] eta_m
         double poly[NB];
 #pragma unroll
         for (int i = 0; i < NB; ++i) poly[i] = 0.0;
         poly[0] = 1.0;
-        int deg = 0;
+        constexpr int f0 = expt(j, 0), f1 = expt(j, 1), f2 = expt(j, 2);
+        constexpr int nfac = f0 + f1 + f2;
+        sfor<nfac>([&](auto r) {
+            constexpr int d = r < f0 ? 0 : (r < f0 + f1 ? 1 : 2);
+            constexpr int deg = r;
+            double np[NB];
 #pragma unroll
-        for (int d = 0; d < 3; ++d) {
-#pragma unroll
-            for (int r = 0; r < expt(j, d); ++r) {
-                double np[NB];
-#pragma unroll
-                for (int i = 0; i < NB; ++i) np[i] = 0.0;
-#pragma unroll
-                for (int i = 0; i < NB; ++i) {
-                    if (expt(i, 0) + expt(i, 1) + expt(i, 2) != deg) continue;
-#pragma unroll
-                    for (int mm = 0; mm < 3; ++mm) {
-                        const int tgt = mono_index(expt(i, 0) + (mm == 0), expt(i, 1) + (mm == 1),
-                                                   expt(i, 2) + (mm == 2));
-                        if (tgt < NB) np[tgt] += poly[i] * M[d * 3 + mm];
-                    }
+            for (int i = 0; i < NB; ++i) np[i] = 0.0;
+            sfor<NB>([&](auto i) {
+                if constexpr (expt(i, 0) + expt(i, 1) + expt(i, 2) == deg) {
+                    sfor<3>([&](auto mm) {
+                        constexpr int tgt =
+                            mono_index(expt(i, 0) + (mm == 0), expt(i, 1) + (mm == 1), expt(i, 2) + (mm == 2));
+                        if constexpr (tgt < NB) np[tgt] += poly[i] * M[d * 3 + mm];
+                    });
                 }
+            });
 #pragma unroll
-                for (int i = 0; i < NB; ++i) poly[i] = np[i];
-                ++deg;
-            }
-        }
+            for (int i = 0; i < NB; ++i) poly[i] = np[i];
+        });
 #pragma unroll
         for (int v = 0; v < 5; ++v) {
             const double cj = in[c * RS + v * NB + j];
 #pragma unroll
             for (int i = 0; i < NB; ++i) o[v][i] += poly[i] * cj;
         }
-    }
+    });
 #pragma unroll
     for (int v = 0; v < 5; ++v)
 #pragma unroll

