@@ -32,8 +32,9 @@
  *    to an even count, in the reference-element monomial basis (see
  *    DESIGN.md; hodg_modal_transform converts to/from the reference's
  *    physical Taylor basis);
- *  - face flux buffer: (F, 5, nqf) at kernel precision (the reference's
- *    FaceFluxBuffer.inviscid, hodg/dg.py:86-92, transposed);
+ *  - face flux buffer: (F, hodg_face_record_stride) at kernel precision,
+ *    record = H[v][q] (the reference's FaceFluxBuffer.inviscid,
+ *    hodg/dg.py:86-92, transposed) padded to 16 bytes;
  *  - geometry: see hodg_mesh_desc.
  */
 #ifndef HODG_B200_H
@@ -64,8 +65,9 @@ extern "C" {
 #define HODG_PREC_F64 64
 #define HODG_PREC_MIXED 32
 
-/* element geometry record, 16 doubles per element */
-#define HODG_EGEO_STRIDE 16 /* Jinv[9] row-major, fc[4] = sgn*area/vol, h, vol, pad */
+/* element geometry record, 16 doubles per element, stored tile-major (see
+ * hodg_elem_tile): fields Jinv[9] row-major, fc[4] = sgn*area/vol, h, vol, pad */
+#define HODG_EGEO_FIELDS 16
 #define HODG_ECONV_STRIDE 18 /* A = J/h [9], A^-1 [9] (modal transforms) */
 
 typedef struct {
@@ -75,9 +77,9 @@ typedef struct {
     int flux_kind;    /* HODG_FLUX_ROE | HODG_FLUX_LLF */
     double gamma;
     double qinf[5];   /* far-field state (conserved) */
-    const double* egeo;      /* (N, 16) */
+    const double* egeo;      /* tile-major (ceil(N/T), 16, T), T = hodg_elem_tile(order) */
     const double* econv;     /* (N, 18) */
-    const int32_t* efaces;   /* (N, 4) face id of local face s (opposite vertex s) */
+    const int32_t* efaces;   /* tile-major (ceil(N/T), 4, T): face id of local face s (opposite vertex s) */
     const int32_t* fcells;   /* (F, 2) left, right (-1 at boundary) */
     const int32_t* finfo;    /* (F,) slotL | slotR << 2 | bc << 4 */
     const double* fnrm;      /* (F, 4) unit normal left->right, pad */
@@ -112,6 +114,13 @@ int hodg_state_row_stride(int order);  /* rs */
 int hodg_n_basis(int order);
 int hodg_n_face_points(int order);
 int hodg_n_vol_points(int order);
+/* elements per element-kernel tile: egeo / efaces are stored tile-major,
+ * egeo[(e / T) * 16 T + field * T + e % T], efaces[(e / T) * 4 T + s * T + e % T],
+ * padded to whole tiles */
+int hodg_elem_tile(int order);
+/* per-face record stride (values of the kernel precision) of the face flux
+ * buffer: 5 x nqf values H[v][q] padded to 16 bytes */
+int hodg_face_record_stride(int order, int prec);
 int64_t hodg_stage_blocks(const hodg_mesh* mesh, int prec); /* rows of norm_partial */
 
 int hodg_face_flux(const hodg_mesh* mesh, int prec, const double* state, void* face_buf, uint32_t* err,

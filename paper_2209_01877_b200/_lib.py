@@ -71,6 +71,8 @@ SIGNATURES = {
     "hodg_n_basis": (I32, [I32]),
     "hodg_n_face_points": (I32, [I32]),
     "hodg_n_vol_points": (I32, [I32]),
+    "hodg_elem_tile": (I32, [I32]),
+    "hodg_face_record_stride": (I32, [I32, I32]),
     "hodg_stage_blocks": (I64, [P, I32]),
     "hodg_face_flux": (I32, [P, I32, P, P, P, P]),
     "hodg_elem_stage": (I32, [P, I32, P, C.POINTER(StageArgs), P, P]),

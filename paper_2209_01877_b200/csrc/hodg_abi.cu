@@ -39,6 +39,7 @@ namespace {
 constexpr int NB_TAB[4] = {1, 4, 10, 20};
 constexpr int NQV_TAB[4] = {1, 4, 14, 24};
 constexpr int NQF_TAB[4] = {1, 6, 7, 15};
+constexpr int TILE_TAB[4] = {64, 64, 32, 16};  // elements per CTA (hodg_kernels.cuh: E)
 
 inline int rs_of(int p) { return (5 * NB_TAB[p] + 1) & ~1; }
 
@@ -46,13 +47,12 @@ inline int rs_of(int p) { return (5 * NB_TAB[p] + 1) & ~1; }
 constexpr int RT = 256;
 
 __global__ void norm_partial_kernel(const double* __restrict__ res, const double* __restrict__ egeo, int64_t n,
-                                    int rs, double* __restrict__ partial) {
+                                    int rs, int nb, int tile, double* __restrict__ partial) {
     __shared__ double sm[5][RT];
     const int64_t c = int64_t(blockIdx.x) * RT + threadIdx.x;
     double v5[5] = {0, 0, 0, 0, 0};
     if (c < n) {
-        const double vol = egeo[c * 16 + 14];
-        const int nb = rs >= 100 ? 20 : (rs >= 50 ? 10 : (rs >= 20 ? 4 : 1));
+        const double vol = egeo[(c / tile) * 16 * tile + 14 * tile + (c % tile)];
         for (int v = 0; v < 5; ++v) {
             const double r = res[c * rs + v * nb];
             v5[v] = vol * r * r;
@@ -117,6 +117,12 @@ int hodg_state_row_stride(int order) { return (order < 0 || order > 3) ? -1 : rs
 int hodg_n_basis(int order) { return (order < 0 || order > 3) ? -1 : NB_TAB[order]; }
 int hodg_n_face_points(int order) { return (order < 0 || order > 3) ? -1 : NQF_TAB[order]; }
 int hodg_n_vol_points(int order) { return (order < 0 || order > 3) ? -1 : NQV_TAB[order]; }
+int hodg_elem_tile(int order) { return (order < 0 || order > 3) ? -1 : TILE_TAB[order]; }
+int hodg_face_record_stride(int order, int prec) {
+    if (order < 0 || order > 3 || (prec != HODG_PREC_F64 && prec != HODG_PREC_MIXED)) return -1;
+    const int sz = prec == HODG_PREC_F64 ? 8 : 4;
+    return int(((5 * NQF_TAB[order] * sz + 15) / 16) * 16 / sz);
+}
 
 int hodg_mesh_create(const hodg_mesh_desc* desc, hodg_mesh** out) {
     if (!desc || !out) return HODG_EINVAL;
@@ -215,7 +221,9 @@ int hodg_residual_l2(const hodg_mesh* mesh, const double* res, double* scratch, 
     const int64_t n = mesh->d.n_elems;
     const int64_t nblk = (n + RT - 1) / RT;
     g_launches += 2;
-    norm_partial_kernel<<<unsigned(nblk), RT, 0, S(stream)>>>(res, mesh->d.egeo, n, rs_of(mesh->d.order), scratch);
+    const int p = mesh->d.order;
+    norm_partial_kernel<<<unsigned(nblk), RT, 0, S(stream)>>>(res, mesh->d.egeo, n, rs_of(p), NB_TAB[p], TILE_TAB[p],
+                                                               scratch);
     norm_finalize_kernel<<<1, RT, 0, S(stream)>>>(scratch, nblk, out5);
     return cudaGetLastError() == cudaSuccess ? HODG_OK : HODG_ECUDA;
 }

@@ -27,6 +27,20 @@ constexpr int FBS = NQF * NB + 1;            // padded per-slot stride of the sm
 constexpr int E = (ORDER >= 3) ? 16 : (ORDER == 2 ? 32 : 64);  // elements per CTA
 constexpr int ETHREADS = 5 * E;
 constexpr int XS = 15;                        // smem slot per (element, qp): 5 traces -> 15 contravariant fluxes
+constexpr int QC = (NQV <= 8) ? NQV : (ORDER == 2 ? 7 : 8);  // volume qps per chunk (bounds the X buffer)
+constexpr int NCH = (NQV + QC - 1) / QC;
+
+// padded per-face record of the face flux buffer: 5 x NQF values rounded up
+// to 16 bytes so each face is one TMA bulk copy
+template <typename T>
+__host__ __device__ constexpr int hstride() {
+    return int(((5 * NQF * sizeof(T) + 15) / 16) * 16 / sizeof(T));
+}
+// smem stride of the gathered face records (2-way worst-case bank pattern)
+template <typename T>
+__host__ __device__ constexpr int hsmem() {
+    return sizeof(T) == 8 ? ((hstride<T>() % 4 == 2) ? hstride<T>() : hstride<T>() + 2) : hstride<T>();
+}
 
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 __host__ __device__ constexpr size_t cmax(size_t a, size_t b) { return a > b ? a : b; }
@@ -64,10 +78,22 @@ __host__ __device__ constexpr size_t face_smem_bytes() {
            align16(cmax(size_t(2 * FT) * RS * sizeof(double), size_t(2 * FT) * NQF * 5 * sizeof(T)));
 }
 
+// element kernel shared memory carve-up
+template <typename T>
+struct ElemSmem {
+    static constexpr size_t bar = 0;                                         // 2 mbarriers
+    static constexpr size_t geo = 16;                                        // 16 x E doubles (tiled)
+    static constexpr size_t fid = geo + size_t(16) * E * 8;                  // 4 x E int32 (tiled)
+    static constexpr size_t red = fid + size_t(4) * E * 4;                   // 10 x E doubles
+    static constexpr size_t htile = align16(red + size_t(10) * E * 8);       // 4 x E face records
+    static constexpr size_t sx = align16(htile + size_t(4) * E * hsmem<T>() * sizeof(T));
+    static constexpr size_t sx_bytes = cmax(size_t(E) * RS * 8, size_t(QC) * E * XS * sizeof(T));
+    static constexpr size_t total = sx + sx_bytes;
+};
+
 template <typename T>
 __host__ __device__ constexpr size_t elem_smem_bytes() {
-    return 16 + size_t(E) * RS * 8 + size_t(E) * 16 * 8 + size_t(E) * 16 + size_t(E) * 10 * 8 +
-           size_t(NQV) * E * XS * sizeof(T) + 16;
+    return ElemSmem<T>::total;
 }
 
 // ---------------------------------------------------------------------------
@@ -79,11 +105,13 @@ __host__ __device__ constexpr size_t elem_smem_bytes() {
 //           slot, staged in smem; coefficients reused across qps, basis values
 //           across the 5 variables);
 //  phase 2: thread (face, qp) closes boundary faces with the BC state and
-//           evaluates the Roe / LLF flux, writing H[f][v][q].
+//           evaluates the Roe / LLF flux, writing H[f][v][q] (padded record).
 template <typename T>
-__global__ void __launch_bounds__(FACE_THREADS) face_flux_kernel(const hodg_mesh_desc m,
-                                                                 const double* __restrict__ state,
-                                                                 T* __restrict__ hbuf, uint32_t* __restrict__ err) {
+__global__ void __launch_bounds__(FACE_THREADS, 3) face_flux_kernel(const hodg_mesh_desc m,
+                                                                    const double* __restrict__ state,
+                                                                    T* __restrict__ hbuf,
+                                                                    uint32_t* __restrict__ err) {
+    constexpr int HS = hstride<T>();
     extern __shared__ __align__(16) unsigned char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
     T* fbt = reinterpret_cast<T*>(smem + 16);
@@ -160,6 +188,7 @@ __global__ void __launch_bounds__(FACE_THREADS) face_flux_kernel(const hodg_mesh
     __syncthreads();
 
     const T gam = T(m.gamma);
+#pragma unroll 2
     for (int p = t; p < nf * NQF; p += FACE_THREADS) {
         const int lfp = p / NQF;
         const int q = p - lfp * NQF;
@@ -190,7 +219,7 @@ __global__ void __launch_bounds__(FACE_THREADS) face_flux_kernel(const hodg_mesh
             for (int v = 0; v < 5; ++v) h[v] = T(0);
         }
 #pragma unroll
-        for (int v = 0; v < 5; ++v) hbuf[(f * 5 + v) * NQF + q] = h[v];
+        for (int v = 0; v < 5; ++v) hbuf[f * HS + v * NQF + q] = h[v];
     }
 }
 
@@ -198,119 +227,161 @@ __global__ void __launch_bounds__(FACE_THREADS) face_flux_kernel(const hodg_mesh
 // Element kernel: hodg/dg.py:353-460 fused with the RK stage update
 // (hodg/timestepping.py:165-180) and the next step's CFL dt
 // (hodg/timestepping.py:105-134).  One CTA = E elements, thread (v, e).
-//  phase 0: TMA bulk copies of the state / geometry / face-id tiles;
-//  phase A: thread (v, e): traces of variable v at the NQV volume points;
-//  phase B: thread (e, q): Euler flux, contravariant flux J^-1 F;
-//  phase C: thread (v, e): volume integral, gather of the 4 face fluxes,
-//           reference mass solve (FP64), RK combination, epilogues.
+//  phase 0: TMA bulk copies of the state / geometry / face-id tiles, then
+//           one bulk copy per (element, face) of the face flux records --
+//           in flight while the volume integral runs;
+//  per chunk of QC volume points:
+//    phase A: thread (v, e): traces of variable v (coefficients in registers);
+//    phase B: thread (e, q): Euler flux, contravariant flux J^-1 F;
+//    phase C: thread (v, e): volume integral (weighted derivative tables);
+//  gather: thread (v, e): the four face fluxes against the face tables,
+//  then the reference mass solve (FP64), RK combination, dt / norm epilogues.
+// Geometry tiles are field-major ([tile][field][E]) so every smem access in
+// the hot phases is unit-stride across the warp.
 template <typename T>
 __global__ void __launch_bounds__(ETHREADS) elem_stage_kernel(const hodg_mesh_desc m, const T* __restrict__ hbuf,
                                                               const hodg_stage_args a, uint32_t* __restrict__ err) {
+    using L = ElemSmem<T>;
+    constexpr int HS = hstride<T>();
+    constexpr int HSS = hsmem<T>();
     extern __shared__ __align__(16) unsigned char smem[];
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
-    double* S = reinterpret_cast<double*>(smem + 16);
-    double* G = S + E * RS;
-    int32_t* FI = reinterpret_cast<int32_t*>(G + E * 16);
-    double* RED = reinterpret_cast<double*>(FI + E * 4);  // [0, 5E): norm terms, [5E, 10E): cell means
-    T* X = reinterpret_cast<T*>(RED + 10 * E);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::bar);
+    double* G = reinterpret_cast<double*>(smem + L::geo);
+    int32_t* FI = reinterpret_cast<int32_t*>(smem + L::fid);
+    double* RED = reinterpret_cast<double*>(smem + L::red);  // [0, 5E): norm terms, [5E, 10E): cell means
+    T* HT = reinterpret_cast<T*>(smem + L::htile);
+    double* S = reinterpret_cast<double*>(smem + L::sx);  // state tile, later the output tile
+    T* X = reinterpret_cast<T*>(smem + L::sx);            // per-chunk trace / flux slots
     __shared__ unsigned long long blk_dt;
 
     const int t = threadIdx.x;
-    const int64_t e0 = int64_t(blockIdx.x) * E;
+    const int64_t tile = blockIdx.x;
+    const int64_t e0 = tile * E;
     const int ne = int(min(int64_t(E), m.n_elems - e0));
     if (t == 0) {
         if (a.dt_reset && blockIdx.x == 0) *a.dt_reset = 0x7FF0000000000000ull;
         blk_dt = 0x7FF0000000000000ull;
         mbar_init(bar, 1);
+        mbar_init(bar + 1, 4 * E);
         mbar_fence_init();
-        const uint32_t bs = uint32_t(ne) * RS * 8, bg = uint32_t(ne) * 16 * 8, bf = uint32_t(ne) * 16;
-        mbar_arrive_expect_tx(bar, bs + bg + bf);
+        const uint32_t bs = uint32_t(ne) * RS * 8;
+        mbar_arrive_expect_tx(bar, bs + 16 * E * 8 + 4 * E * 4);
         bulk_g2s(S, a.us + e0 * RS, bs, bar);
-        bulk_g2s(G, m.egeo + e0 * 16, bg, bar);
-        bulk_g2s(FI, m.efaces + e0 * 4, bf, bar);
+        bulk_g2s(G, m.egeo + tile * 16 * E, 16 * E * 8, bar);
+        bulk_g2s(FI, m.efaces + tile * 4 * E, 4 * E * 4, bar);
     }
     __syncthreads();
     mbar_wait(bar, 0);
 
     const int v = t / E;
     const int e = t - v * E;
-
-    // phase A: volume traces of variable v
-    if (e < ne) {
-        T c[NB];
-#pragma unroll
-        for (int i = 0; i < NB; ++i) c[i] = T(S[e * RS + v * NB + i]);
-        sfor<NQV>([&](auto q) {
-            T u = T(0);
-            sfor<NB>([&](auto i) { u += TAB(VB, T, q * NB + i) * c[i]; });
-            X[(q * E + e) * XS + v] = u;
-        });
-    }
-    __syncthreads();
-
-    // phase B: flux and contravariant flux at each (element, qp)
-    const T gam = T(m.gamma);
-    for (int p = t; p < E * NQV; p += ETHREADS) {
-        const int q = p / E;
-        const int ee = p - q * E;
-        if (ee >= ne) continue;
-        T* sl = X + (q * E + ee) * XS;
-        T U[5];
-#pragma unroll
-        for (int k = 0; k < 5; ++k) U[k] = sl[k];
-        T u, vv, w;
-        const T pr = (U[0] > T(0)) ? prim(U, gam, u, vv, w) : T(-1);
-        if (!(pr > T(0))) {
-            flag(err, 1, uint32_t(e0 + ee));
-#pragma unroll
-            for (int k = 0; k < XS; ++k) sl[k] = T(0);
-            continue;
-        }
-        const T Hs = U[4] + pr;
-        const T F[3][5] = {{U[1], U[1] * u + pr, U[1] * vv, U[1] * w, Hs * u},
-                           {U[2], U[2] * u, U[2] * vv + pr, U[2] * w, Hs * vv},
-                           {U[3], U[3] * u, U[3] * vv, U[3] * w + pr, Hs * w}};
-        const double* Ji = G + ee * 16;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            const T j0 = T(Ji[3 * k]), j1 = T(Ji[3 * k + 1]), j2 = T(Ji[3 * k + 2]);
-#pragma unroll
-            for (int c = 0; c < 5; ++c) sl[k * 5 + c] = j0 * F[0][c] + j1 * F[1][c] + j2 * F[2][c];
+    // face flux records: thread (s, e) for t < 4E fetches face FI[s][e]
+    if (t < 4 * E) {
+        const int ee = t % E;
+        if (ee < ne) {
+            const int64_t f = FI[t];
+            mbar_arrive_expect_tx(bar + 1, HS * sizeof(T));
+            bulk_g2s(HT + size_t(t) * HSS, hbuf + f * HS, HS * sizeof(T), bar + 1);
+        } else {
+            mbar_arrive(bar + 1);
         }
     }
-    __syncthreads();
 
-    // phase C
     const int64_t gid = e0 + e;
-    if (e < ne) {
-        T acc[NB];
+    const bool live = e < ne;
+    const bool need_u0 = a.combine == 1 || (a.combine == 0 && a.a != 0.0);
+    double c[NB];
+    double u0r[(ORDER <= 2) ? NB : 1];
+    if (live) {
 #pragma unroll
-        for (int i = 0; i < NB; ++i) acc[i] = T(0);
-        sfor<NQV>([&](auto q) {
-            const T* sl = X + (q * E + e) * XS;
-            const T fd[3] = {sl[v], sl[5 + v], sl[10 + v]};
-            sfor<NB>([&](auto i) {
-                sfor<3>([&](auto d) {
-                    if constexpr (expt(i, d) > 0) acc[i] += TAB(VD, T, (q * NB + i) * 3 + d) * fd[d];
+        for (int i = 0; i < NB; ++i) c[i] = S[e * RS + v * NB + i];
+        if constexpr (ORDER <= 2) {
+            if (need_u0) {
+#pragma unroll
+                for (int i = 0; i < NB; ++i) u0r[i] = a.u0[gid * RS + v * NB + i];
+            }
+        }
+    }
+    __syncthreads();  // state tile consumed: the region now holds X
+
+    T acc[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) acc[i] = T(0);
+    const T gam = T(m.gamma);
+    sfor<NCH>([&](auto ch) {
+        constexpr int q0 = ch * QC;
+        constexpr int nq = (NQV - q0) < QC ? (NQV - q0) : QC;
+        // phase A
+        if (live) {
+            sfor<nq>([&](auto qq) {
+                T u = T(0);
+                sfor<NB>([&](auto i) { u += TAB(VB, T, (q0 + qq) * NB + i) * T(c[i]); });
+                X[(qq * E + e) * XS + v] = u;
+            });
+        }
+        __syncthreads();
+        // phase B
+        for (int p = t; p < nq * E; p += ETHREADS) {
+            const int qq = p / E;
+            const int ee = p - qq * E;
+            if (ee >= ne) continue;
+            T* sl = X + (qq * E + ee) * XS;
+            T U[5];
+#pragma unroll
+            for (int k = 0; k < 5; ++k) U[k] = sl[k];
+            T u, vv, w;
+            const T pr = (U[0] > T(0)) ? prim(U, gam, u, vv, w) : T(-1);
+            if (!(pr > T(0))) {
+                flag(err, 1, uint32_t(e0 + ee));
+#pragma unroll
+                for (int k = 0; k < XS; ++k) sl[k] = T(0);
+                continue;
+            }
+            const T Hs = U[4] + pr;
+            const T F[3][5] = {{U[1], U[1] * u + pr, U[1] * vv, U[1] * w, Hs * u},
+                               {U[2], U[2] * u, U[2] * vv + pr, U[2] * w, Hs * vv},
+                               {U[3], U[3] * u, U[3] * vv, U[3] * w + pr, Hs * w}};
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const T j0 = T(G[(3 * k) * E + ee]), j1 = T(G[(3 * k + 1) * E + ee]), j2 = T(G[(3 * k + 2) * E + ee]);
+#pragma unroll
+                for (int cc = 0; cc < 5; ++cc) sl[k * 5 + cc] = j0 * F[0][cc] + j1 * F[1][cc] + j2 * F[2][cc];
+            }
+        }
+        __syncthreads();
+        // phase C (volume)
+        if (live) {
+            sfor<nq>([&](auto qq) {
+                const T* sl = X + (qq * E + e) * XS;
+                const T fd[3] = {sl[v], sl[5 + v], sl[10 + v]};
+                sfor<NB>([&](auto i) {
+                    sfor<3>([&](auto d) {
+                        if constexpr (expt(i, d) > 0) acc[i] += TAB(VD, T, ((q0 + qq) * NB + i) * 3 + d) * fd[d];
+                    });
                 });
             });
-        });
+        }
+        __syncthreads();
+    });
+
+    // face gather, mass solve, RK update
+    mbar_wait(bar + 1, 0);
+    if (live) {
         double accd[NB];
 #pragma unroll
         for (int i = 0; i < NB; ++i) accd[i] = double(acc[i]);
         sfor<4>([&](auto s) {
-            const int64_t f = FI[e * 4 + s];
-            const T* H = hbuf + (f * 5 + v) * NQF;
+            const T* hrec = HT + size_t(s * E + e) * HSS + v * NQF;
             T hq[NQF];
 #pragma unroll
-            for (int q = 0; q < NQF; ++q) hq[q] = __ldg(H + q);
+            for (int q = 0; q < NQF; ++q) hq[q] = hrec[q];
             T fa[NB];
 #pragma unroll
             for (int i = 0; i < NB; ++i) fa[i] = T(0);
             sfor<NQF>([&](auto q) {
                 sfor<NB>([&](auto i) { fa[i] += TAB(FG, T, (s * NQF + q) * NB + i) * hq[q]; });
             });
-            const double fc = G[e * 16 + 9 + s];
+            const double fc = G[(9 + s) * E + e];
 #pragma unroll
             for (int i = 0; i < NB; ++i) accd[i] -= fc * double(fa[i]);
         });
@@ -324,18 +395,22 @@ __global__ void __launch_bounds__(ETHREADS) elem_stage_kernel(const hodg_mesh_de
 #pragma unroll
             for (int j = 0; j < NB; ++j) a.res[gid * RS + v * NB + j] = r[j];
         }
-        if (a.norm_partial) RED[v * E + e] = G[e * 16 + 14] * r[0] * r[0];
+        if (a.norm_partial) RED[v * E + e] = G[14 * E + e] * r[0] * r[0];
         if (a.combine >= 0) {
             const double dt = a.dt_is_vector ? a.dt[gid] : a.dt[0];
             double mean = 0.0;
             sfor<NB>([&](auto j) {
-                const double us = S[e * RS + v * NB + j];
+                double u0j = 0.0;
+                if (need_u0) {
+                    if constexpr (ORDER <= 2) u0j = u0r[j];
+                    else u0j = a.u0[gid * RS + v * NB + j];
+                }
                 double o;
                 if (a.combine == 1) {
-                    o = 0.5 * ((a.u0[gid * RS + v * NB + j] + us) + dt * r[j]);
+                    o = 0.5 * ((u0j + c[j]) + dt * r[j]);
                 } else {
-                    o = a.b * (us + dt * r[j]);
-                    if (a.a != 0.0) o = a.a * a.u0[gid * RS + v * NB + j] + o;
+                    o = a.b * (c[j] + dt * r[j]);
+                    if (a.a != 0.0) o = a.a * u0j + o;
                 }
                 S[e * RS + v * NB + j] = o;
                 mean += MEAN_T[j] * o;
@@ -364,10 +439,8 @@ __global__ void __launch_bounds__(ETHREADS) elem_stage_kernel(const hodg_mesh_de
             if (!(p > 0.0)) {
                 flag(err, 2, uint32_t(e0 + t));
             } else {
-                const double fac = 2.0 * ORDER + 1.0;
-                const double h = G[t * 16 + 13];
                 const double speed = sqrt(u * u + vv * vv + w * w) + sqrt(m.gamma * p / m0);
-                dt = a.cfl * h / (fac * speed);
+                dt = a.cfl * G[13 * E + t] / ((2.0 * ORDER + 1.0) * speed);
                 if (a.dt_next) atomicMin(&blk_dt, static_cast<unsigned long long>(__double_as_longlong(dt)));
             }
         }
@@ -404,7 +477,7 @@ __global__ void local_dt_kernel(const hodg_mesh_desc m, const double* __restrict
             flag(err, 2, uint32_t(c));
         } else {
             const double speed = sqrt(u * u + vv * vv + w * w) + sqrt(m.gamma * p / mm[0]);
-            dt = cfl * m.egeo[c * 16 + 13] / ((2.0 * ORDER + 1.0) * speed);
+            dt = cfl * m.egeo[(c / E) * 16 * E + 13 * E + (c % E)] / ((2.0 * ORDER + 1.0) * speed);
             if (dt_min) atomicMin(dt_min, static_cast<unsigned long long>(__double_as_longlong(dt)));
         }
     }

@@ -161,7 +161,8 @@ class Discretization:
         b = self._hbuf.get(prec)
         if b is None:
             dt = torch.float32 if prec == _lib.PREC_MIXED else torch.float64
-            b = torch.empty((self.nf, N_VARS, self.nqf), dtype=dt, device=self.device)
+            hs = int(self.L.hodg_face_record_stride(self.order, prec))
+            b = torch.zeros((self.nf, hs), dtype=dt, device=self.device)
             self._hbuf[prec] = b
         return b
 
@@ -278,7 +279,8 @@ def face_flux_pass(state: DofState, aux, mesh: TetMesh, geo: DeviceGeometry, bcs
     disc.reset_errors()
     hbuf = disc.face_flux(rows, prec, hbuf=_torch().empty_like(disc.face_buffer(prec)))
     disc.raise_errors(state.iteration)
-    return FaceFluxBuffer(inviscid=hbuf.transpose(1, 2))
+    h = hbuf[:, : N_VARS * disc.nqf].reshape(disc.nf, N_VARS, disc.nqf)
+    return FaceFluxBuffer(inviscid=h.transpose(1, 2))
 
 
 def accumulate_rhs(state: DofState, aux, fluxes: FaceFluxBuffer, mesh: TetMesh, geo: DeviceGeometry,
@@ -289,7 +291,9 @@ def accumulate_rhs(state: DofState, aux, fluxes: FaceFluxBuffer, mesh: TetMesh, 
     prec = _prec_of(state)
     rows = disc.to_reference(state.coeffs)
     dt = torch.float32 if prec == _lib.PREC_MIXED else torch.float64
-    hbuf = torch.as_tensor(fluxes.inviscid, device=disc.device).to(dt).transpose(1, 2).contiguous()
+    hbuf = torch.zeros_like(disc.face_buffer(prec))
+    hbuf[:, : N_VARS * disc.nqf] = torch.as_tensor(fluxes.inviscid, device=disc.device).to(dt).transpose(
+        1, 2).reshape(disc.nf, -1)
     disc.reset_errors()
     res = disc.residual_rows(rows, hbuf, prec)
     disc.raise_errors(state.iteration)

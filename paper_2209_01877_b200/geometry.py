@@ -4,10 +4,14 @@ Replaces the reference's per-cell x per-quadrature-point tables
 (`hodg/geometry.py:33-220`; about 8 GB at one million P2 tetrahedra) by
 16 doubles per element and 4 per face:
 
-  egeo  (N, 16): J^-1 (row-major, 9), fc[s] = sgn_s * area_s / vol (4), h, vol, 0
+  egeo  16 fields: J^-1 (row-major, 9), fc[s] = sgn_s * area_s / vol (4), h, vol, 0
   econv (N, 18): A = J / h and A^-1 (modal transforms to/from the Taylor basis)
-  efaces (N, 4): face id of local face s
+  efaces 4 fields: face id of local face s
   fcells (F, 2), finfo (F,) = slotL | slotR << 2 | bc << 4, fnrm (F, 4)
+
+egeo and efaces are stored tile-major, [tile][field][T] with T elements per
+element-kernel CTA (TILE below == hodg_elem_tile), so one tile is one TMA
+bulk copy and every per-field shared-memory read is unit-stride.
 
 with J = [V1 - V0, V2 - V0, V3 - V0] (vertices ascending) the affine map of
 the reference tetrahedron.  Everything else is a compile-time constant of
@@ -23,7 +27,18 @@ import numpy as np
 from .mesh import TetMesh
 from .refelem import ref_tables
 
-__all__ = ["GeometryError", "DeviceGeometry", "compute_geometry", "volume_points"]
+__all__ = ["GeometryError", "DeviceGeometry", "compute_geometry", "volume_points", "TILE", "tile_major"]
+
+TILE = {0: 64, 1: 64, 2: 32, 3: 16}  # elements per element-kernel CTA (hodg_kernels.cuh: E)
+
+
+def tile_major(a: np.ndarray, tile: int) -> np.ndarray:
+    """(N, F) -> flat [ceil(N/tile)][F][tile], zero padded."""
+    n, nf = a.shape
+    nt = (n + tile - 1) // tile
+    pad = np.zeros((nt * tile, nf), dtype=a.dtype)
+    pad[:n] = a
+    return np.ascontiguousarray(pad.reshape(nt, tile, nf).transpose(0, 2, 1)).ravel()
 
 
 class GeometryError(Exception):
@@ -99,8 +114,10 @@ def compute_geometry(mesh: TetMesh, order: int) -> DeviceGeometry:
     finfo = (slots[:, 0] | (np.maximum(slots[:, 1], 0) << 2) | (codes.astype(np.int32) << 4)).astype(np.int32)
     fnrm = np.zeros((mesh.n_faces, 4))
     fnrm[:, :3] = mesh.face_normal
-    return DeviceGeometry(order, ref_tables(order).nb, egeo, econv, mesh.cell_faces.astype(np.int32),
-                          mesh.face_cells.astype(np.int32), finfo, fnrm)
+    T = TILE[order]
+    return DeviceGeometry(order, ref_tables(order).nb, tile_major(egeo, T), econv,
+                          tile_major(mesh.cell_faces.astype(np.int32), T), mesh.face_cells.astype(np.int32), finfo,
+                          fnrm)
 
 
 def volume_points(mesh: TetMesh, order: int) -> np.ndarray:

@@ -38,6 +38,11 @@ def test_host_side_argument_checks():
     assert [L.hodg_n_basis(p) for p in range(4)] == [1, 4, 10, 20]
     assert [L.hodg_state_row_stride(p) for p in range(4)] == [6, 20, 50, 100]
     assert L.hodg_n_basis(4) == -1
+    from paper_2209_01877_b200.geometry import TILE
+
+    assert [L.hodg_elem_tile(p) for p in range(4)] == [TILE[p] for p in range(4)]
+    assert [L.hodg_face_record_stride(p, 64) for p in range(4)] == [6, 30, 36, 76]
+    assert [L.hodg_face_record_stride(p, 32) for p in range(4)] == [8, 32, 36, 76]
     h = C.c_void_p()
     d = _lib.MeshDesc()
     d.order = 7
