@@ -19,10 +19,10 @@ namespace hodg {
 namespace HODG_CAT(ord, ORDER) {
 
 constexpr int RS = (5 * NB + 1) & ~1;        // state row stride (doubles)
-constexpr int NG = (NQF > 8) ? 2 : 1;        // face qp groups per side thread
+constexpr int NG = (NQF > 1) ? 2 : 1;        // face qp groups per side thread
 constexpr int QPT = (NQF + NG - 1) / NG;     // face qps per phase-1 thread
 constexpr int FACE_THREADS = 128;
-constexpr int FT = FACE_THREADS / (2 * NG);  // faces per CTA
+constexpr int FT = FACE_THREADS / (2 * NG);  // faces per CTA (32 for P1-P3)
 constexpr int FBS = NQF * NB + 1;            // padded per-slot stride of the smem trace table
 constexpr int E = (ORDER >= 3) ? 16 : (ORDER == 2 ? 32 : 64);  // elements per CTA
 constexpr int ETHREADS = 5 * E;
@@ -107,7 +107,7 @@ __host__ __device__ constexpr size_t elem_smem_bytes() {
 //  phase 2: thread (face, qp) closes boundary faces with the BC state and
 //           evaluates the Roe / LLF flux, writing H[f][v][q] (padded record).
 template <typename T>
-__global__ void __launch_bounds__(FACE_THREADS, 3) face_flux_kernel(const hodg_mesh_desc m,
+__global__ void __launch_bounds__(FACE_THREADS, 4) face_flux_kernel(const hodg_mesh_desc m,
                                                                     const double* __restrict__ state,
                                                                     T* __restrict__ hbuf,
                                                                     uint32_t* __restrict__ err) {
@@ -117,6 +117,8 @@ __global__ void __launch_bounds__(FACE_THREADS, 3) face_flux_kernel(const hodg_m
     T* fbt = reinterpret_cast<T*>(smem + 16);
     double* rows = reinterpret_cast<double*>(smem + align16(16 + 4 * FBS * sizeof(T)));
     T* trs = reinterpret_cast<T*>(rows);  // aliases rows after phase 1
+    __shared__ double fn[FT][3];
+    __shared__ int finf[FT];
 
     const int t = threadIdx.x;
     const int64_t f0 = int64_t(blockIdx.x) * FT;
@@ -132,6 +134,14 @@ __global__ void __launch_bounds__(FACE_THREADS, 3) face_flux_kernel(const hodg_m
         elem = m.fcells[2 * (f0 + lf) + side];
         const int info = m.finfo[f0 + lf];
         slot = side == 0 ? (info & 3) : ((info >> 2) & 3);
+        if (side == 0 && g == 0) {
+            // per-face data for phase 2: bc code and a right-side flag, normal
+            finf[lf] = ((info >> 4) & 15) | (m.fcells[2 * (f0 + lf) + 1] >= 0 ? 0x100 : 0);
+            const double4 nn = reinterpret_cast<const double4*>(m.fnrm)[f0 + lf];
+            fn[lf][0] = nn.x;
+            fn[lf][1] = nn.y;
+            fn[lf][2] = nn.z;
+        }
     }
     if (t == 0) {
         mbar_init(bar, FACE_THREADS);
@@ -151,13 +161,14 @@ __global__ void __launch_bounds__(FACE_THREADS, 3) face_flux_kernel(const hodg_m
     }
     mbar_wait(bar, 0);
 
+    // phase 1: traces of this side at qps [g*QPT, g*QPT + QPT)
     T tr[QPT][5];
 #pragma unroll
     for (int qq = 0; qq < QPT; ++qq)
 #pragma unroll
         for (int v = 0; v < 5; ++v) tr[qq][v] = T(0);
     if (elem >= 0) {
-        const T* fb = fbt + slot * FBS;
+        const T* fb = fbt + slot * FBS + g * QPT * NB;
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
             T c[5];
@@ -165,9 +176,8 @@ __global__ void __launch_bounds__(FACE_THREADS, 3) face_flux_kernel(const hodg_m
             for (int v = 0; v < 5; ++v) c[v] = T(myrow[v * NB + i]);
 #pragma unroll
             for (int qq = 0; qq < QPT; ++qq) {
-                const int q = g * QPT + qq;
-                if (NG * QPT == NQF || q < NQF) {
-                    const T b = fb[q * NB + i];
+                if (NG * QPT == NQF || g * QPT + qq < NQF) {
+                    const T b = fb[qq * NB + i];
 #pragma unroll
                     for (int v = 0; v < 5; ++v) tr[qq][v] += b * c[v];
                 }
@@ -187,20 +197,19 @@ __global__ void __launch_bounds__(FACE_THREADS, 3) face_flux_kernel(const hodg_m
     }
     __syncthreads();
 
+    // phase 2: Riemann flux at each (face, qp)
     const T gam = T(m.gamma);
-#pragma unroll 2
     for (int p = t; p < nf * NQF; p += FACE_THREADS) {
         const int lfp = p / NQF;
         const int q = p - lfp * NQF;
         const int64_t f = f0 + lfp;
-        const int bc = (m.finfo[f] >> 4) & 15;
-        const double4 nn = reinterpret_cast<const double4*>(m.fnrm)[f];
-        const T n[3] = {T(nn.x), T(nn.y), T(nn.z)};
+        const int info = finf[lfp];
+        const T n[3] = {T(fn[lfp][0]), T(fn[lfp][1]), T(fn[lfp][2])};
         T qL[5], qR[5], h[5];
 #pragma unroll
         for (int v = 0; v < 5; ++v) qL[v] = trs[(size_t(lfp) * NQF + q) * 5 + v];
         bool ok = true;
-        if (m.fcells[2 * f + 1] >= 0) {
+        if (info & 0x100) {
 #pragma unroll
             for (int v = 0; v < 5; ++v) qR[v] = trs[(size_t(FT + lfp) * NQF + q) * 5 + v];
         } else {
@@ -209,7 +218,7 @@ __global__ void __launch_bounds__(FACE_THREADS, 3) face_flux_kernel(const hodg_m
                 ok = false;
             } else {
                 const T qf[5] = {T(m.qinf[0]), T(m.qinf[1]), T(m.qinf[2]), T(m.qinf[3]), T(m.qinf[4])};
-                bstate(bc, qL, n, qf, gam, qR);
+                bstate(info & 15, qL, n, qf, gam, qR);
             }
         }
         if (ok) ok = (m.flux_kind == HODG_FLUX_LLF) ? llf(qL, qR, n, gam, h) : roe(qL, qR, n, gam, h);
