@@ -108,59 +108,67 @@ __device__ __forceinline__ T prim(const T q[5], T g, T& u, T& v, T& w) {
     return (g - K<T>::one) * (q[4] - K<T>::half * q[0] * (u * u + v * v + w * w));
 }
 
-// Roe flux with Harten-Hyman entropy fix; hodg/physics.py:177-250 (3D)
+// Roe flux with Harten-Hyman entropy fix; hodg/physics.py:177-250 (3D).
+// Straight-line (no early returns, entropy fix as selects) so two calls
+// interleave; divisions are replaced by reciprocals of rho, (sL + sR) and
+// rsqrt(a2).  Returns ok = 0 on rho <= 0, p <= 0 or a2 <= 0 (then f is
+// garbage and the caller flags the face, as the reference's ok = 0).
 template <typename T>
 __device__ __forceinline__ bool roe(const T qL[5], const T qR[5], const T n[3], T g, T f[5]) {
-    const T one = K<T>::one, half = K<T>::half, two = K<T>::two;
-    if (!(qL[0] > K<T>::zero) || !(qR[0] > K<T>::zero)) return false;
-    T uL, vL, wL, uR, vR, wR;
-    T pL = prim(qL, g, uL, vL, wL);
-    T pR = prim(qR, g, uR, vR, wR);
-    if (!(pL > K<T>::zero) || !(pR > K<T>::zero)) return false;
+    const T one = K<T>::one, half = K<T>::half;
+    const T riL = one / qL[0], riR = one / qR[0];
+    const T uL = qL[1] * riL, vL = qL[2] * riL, wL = qL[3] * riL;
+    const T uR = qR[1] * riR, vR = qR[2] * riR, wR = qR[3] * riR;
+    const T gm1 = g - one;
+    const T pL = gm1 * (qL[4] - half * qL[0] * (uL * uL + vL * vL + wL * wL));
+    const T pR = gm1 * (qR[4] - half * qR[0] * (uR * uR + vR * vR + wR * wR));
     const T nx = n[0], ny = n[1], nz = n[2];
-    T vnL = uL * nx + vL * ny + wL * nz;
-    T vnR = uR * nx + vR * ny + wR * nz;
-    T sL = sqrt(qL[0]);
-    T sR = sqrt(qR[0]);
-    T di = one / (sL + sR);
-    T ut = (sL * uL + sR * uR) * di;
-    T vt = (sL * vL + sR * vR) * di;
-    T wt = (sL * wL + sR * wR) * di;
-    T HL = (qL[4] + pL) / qL[0];
-    T HR = (qR[4] + pR) / qR[0];
-    T Ht = (sL * HL + sR * HR) * di;
-    T ke = half * (ut * ut + vt * vt + wt * wt);
-    T a2 = (g - one) * (Ht - ke);
-    if (!(a2 > K<T>::zero)) return false;
-    T a = sqrt(a2);
-    T rt = sL * sR;
-    T unt = ut * nx + vt * ny + wt * nz;
-    T dr = qR[0] - qL[0];
-    T dp = pR - pL;
-    T du = uR - uL, dv = vR - vL, dw = wR - wL;
-    T dun = vnR - vnL;
-    T l1 = fabs(unt - a), l2 = fabs(unt), l4 = fabs(unt + a);
-    T delta = K<T>::efix * a;
-    if (l1 < delta) l1 = half * (l1 * l1 / delta + delta);
-    if (l4 < delta) l4 = half * (l4 * l4 / delta + delta);
-    T ia2 = one / a2;
-    T rad = rt * a * dun;
-    T a1 = (dp - rad) * (half * ia2);
-    T a4 = (dp + rad) * (half * ia2);
-    T a2w = dr - dp * ia2;
-    T w1 = l1 * a1, w4 = l4 * a4;
-    T d0 = w1 + l2 * a2w + w4;
-    T d1 = w1 * (ut - a * nx) + l2 * (a2w * ut + rt * (du - dun * nx)) + w4 * (ut + a * nx);
-    T d2 = w1 * (vt - a * ny) + l2 * (a2w * vt + rt * (dv - dun * ny)) + w4 * (vt + a * ny);
-    T d3 = w1 * (wt - a * nz) + l2 * (a2w * wt + rt * (dw - dun * nz)) + w4 * (wt + a * nz);
-    T dE = w1 * (Ht - a * unt) + l2 * (a2w * ke + rt * (ut * du + vt * dv + wt * dw - unt * dun)) +
-           w4 * (Ht + a * unt);
-    f[0] = half * (qL[0] * vnL + qR[0] * vnR) - half * d0;
-    f[1] = half * (qL[1] * vnL + pL * nx + qR[1] * vnR + pR * nx) - half * d1;
-    f[2] = half * (qL[2] * vnL + pL * ny + qR[2] * vnR + pR * ny) - half * d2;
-    f[3] = half * (qL[3] * vnL + pL * nz + qR[3] * vnR + pR * nz) - half * d3;
-    f[4] = half * ((qL[4] + pL) * vnL + (qR[4] + pR) * vnR) - half * dE;
-    return true;
+    const T vnL = uL * nx + vL * ny + wL * nz;
+    const T vnR = uR * nx + vR * ny + wR * nz;
+    const T sL = sqrt(qL[0]);
+    const T sR = sqrt(qR[0]);
+    const T di = one / (sL + sR);
+    const T ut = (sL * uL + sR * uR) * di;
+    const T vt = (sL * vL + sR * vR) * di;
+    const T wt = (sL * wL + sR * wR) * di;
+    const T HL = (qL[4] + pL) * riL;
+    const T HR = (qR[4] + pR) * riR;
+    const T Ht = (sL * HL + sR * HR) * di;
+    const T ke = half * (ut * ut + vt * vt + wt * wt);
+    const T a2 = gm1 * (Ht - ke);
+    const bool ok = (qL[0] > T(0)) & (qR[0] > T(0)) & (pL > T(0)) & (pR > T(0)) & (a2 > T(0));
+    const T ra = rsqrt(a2);
+    const T a = a2 * ra;
+    const T rt = sL * sR;
+    const T unt = ut * nx + vt * ny + wt * nz;
+    const T dr = qR[0] - qL[0];
+    const T dp = pR - pL;
+    const T du = uR - uL, dv = vR - vL, dw = wR - wL;
+    const T dun = vnR - vnL;
+    T l1 = fabs(unt - a), l4 = fabs(unt + a);
+    const T l2 = fabs(unt);
+    const T delta = K<T>::efix * a;
+    const T idelta = (one / K<T>::efix) * ra;
+    l1 = (l1 < delta) ? half * (l1 * l1 * idelta + delta) : l1;
+    l4 = (l4 < delta) ? half * (l4 * l4 * idelta + delta) : l4;
+    const T ia2h = half * ra * ra;
+    const T rad = rt * a * dun;
+    const T a1 = (dp - rad) * ia2h;
+    const T a4 = (dp + rad) * ia2h;
+    const T a2w = dr - dp * (ra * ra);
+    const T w1 = l1 * a1, w4 = l4 * a4;
+    const T d0 = w1 + l2 * a2w + w4;
+    const T d1 = w1 * (ut - a * nx) + l2 * (a2w * ut + rt * (du - dun * nx)) + w4 * (ut + a * nx);
+    const T d2 = w1 * (vt - a * ny) + l2 * (a2w * vt + rt * (dv - dun * ny)) + w4 * (vt + a * ny);
+    const T d3 = w1 * (wt - a * nz) + l2 * (a2w * wt + rt * (dw - dun * nz)) + w4 * (wt + a * nz);
+    const T dE = w1 * (Ht - a * unt) + l2 * (a2w * ke + rt * (ut * du + vt * dv + wt * dw - unt * dun)) +
+                 w4 * (Ht + a * unt);
+    f[0] = half * (qL[0] * vnL + qR[0] * vnR - d0);
+    f[1] = half * (qL[1] * vnL + qR[1] * vnR + (pL + pR) * nx - d1);
+    f[2] = half * (qL[2] * vnL + qR[2] * vnR + (pL + pR) * ny - d2);
+    f[3] = half * (qL[3] * vnL + qR[3] * vnR + (pL + pR) * nz - d3);
+    f[4] = half * ((qL[4] + pL) * vnL + (qR[4] + pR) * vnR - dE);
+    return ok;
 }
 
 // local Lax-Friedrichs (Rusanov) flux

@@ -26,8 +26,8 @@ constexpr int FT = FACE_THREADS / (2 * NG);  // faces per CTA (32 for P1-P3)
 constexpr int FBS = NQF * NB + 1;            // padded per-slot stride of the smem trace table
 constexpr int E = (ORDER >= 3) ? 16 : (ORDER == 2 ? 32 : 64);  // elements per CTA
 constexpr int ETHREADS = 5 * E;
-constexpr int XS = 15;                        // smem slot per (element, qp): 5 traces -> 15 contravariant fluxes
-constexpr int QC = (NQV <= 8) ? NQV : (ORDER == 2 ? 7 : 8);  // volume qps per chunk (bounds the X buffer)
+constexpr int XS = 5;                         // smem slot per (element, qp): the 5 traces
+constexpr int QC = (NQV <= 14) ? NQV : 12;  // volume qps per chunk (bounds the X buffer)
 constexpr int NCH = (NQV + QC - 1) / QC;
 
 // padded per-face record of the face flux buffer: 5 x NQF values rounded up
@@ -197,38 +197,63 @@ __global__ void __launch_bounds__(FACE_THREADS, 4) face_flux_kernel(const hodg_m
     }
     __syncthreads();
 
-    // phase 2: Riemann flux at each (face, qp)
+    // phase 2: Riemann flux at each (face, qp); two pairs per thread per
+    // iteration so their (straight-line) Roe evaluations interleave
     const T gam = T(m.gamma);
-    for (int p = t; p < nf * NQF; p += FACE_THREADS) {
-        const int lfp = p / NQF;
-        const int q = p - lfp * NQF;
-        const int64_t f = f0 + lfp;
-        const int info = finf[lfp];
-        const T n[3] = {T(fn[lfp][0]), T(fn[lfp][1]), T(fn[lfp][2])};
-        T qL[5], qR[5], h[5];
+    const int npairs = nf * NQF;
+    for (int p0 = t; p0 < npairs; p0 += 2 * FACE_THREADS) {
+        T qL[2][5], qR[2][5], h[2][5], n[2][3];
+        bool ok[2];
+        int64_t fid[2];
+        int qv[2];
 #pragma unroll
-        for (int v = 0; v < 5; ++v) qL[v] = trs[(size_t(lfp) * NQF + q) * 5 + v];
-        bool ok = true;
-        if (info & 0x100) {
+        for (int k = 0; k < 2; ++k) {
+            const int p = min(p0 + k * FACE_THREADS, npairs - 1);
+            const int lfp = p / NQF;
+            const int q = p - lfp * NQF;
+            fid[k] = f0 + lfp;
+            qv[k] = q;
+            const int info = finf[lfp];
 #pragma unroll
-            for (int v = 0; v < 5; ++v) qR[v] = trs[(size_t(FT + lfp) * NQF + q) * 5 + v];
-        } else {
-            T u, vv, w;
-            if (!(qL[0] > T(0)) || !(prim(qL, gam, u, vv, w) > T(0))) {
-                ok = false;
+            for (int d = 0; d < 3; ++d) n[k][d] = T(fn[lfp][d]);
+#pragma unroll
+            for (int v = 0; v < 5; ++v) qL[k][v] = trs[(size_t(lfp) * NQF + q) * 5 + v];
+            ok[k] = true;
+            if (info & 0x100) {
+#pragma unroll
+                for (int v = 0; v < 5; ++v) qR[k][v] = trs[(size_t(FT + lfp) * NQF + q) * 5 + v];
             } else {
-                const T qf[5] = {T(m.qinf[0]), T(m.qinf[1]), T(m.qinf[2]), T(m.qinf[3]), T(m.qinf[4])};
-                bstate(info & 15, qL, n, qf, gam, qR);
+                T u, vv, w;
+                if (!(qL[k][0] > T(0)) || !(prim(qL[k], gam, u, vv, w) > T(0))) {
+                    ok[k] = false;
+#pragma unroll
+                    for (int v = 0; v < 5; ++v) qR[k][v] = qL[k][v];
+                } else {
+                    const T qf[5] = {T(m.qinf[0]), T(m.qinf[1]), T(m.qinf[2]), T(m.qinf[3]), T(m.qinf[4])};
+                    bstate(info & 15, qL[k], n[k], qf, gam, qR[k]);
+                }
             }
         }
-        if (ok) ok = (m.flux_kind == HODG_FLUX_LLF) ? llf(qL, qR, n, gam, h) : roe(qL, qR, n, gam, h);
-        if (!ok) {
-            flag(err, 0, uint32_t(f));
+        if (m.flux_kind == HODG_FLUX_LLF) {
 #pragma unroll
-            for (int v = 0; v < 5; ++v) h[v] = T(0);
+            for (int k = 0; k < 2; ++k) ok[k] = ok[k] && llf(qL[k], qR[k], n[k], gam, h[k]);
+        } else {
+            const bool r0 = roe(qL[0], qR[0], n[0], gam, h[0]);
+            const bool r1 = roe(qL[1], qR[1], n[1], gam, h[1]);
+            ok[0] = ok[0] && r0;
+            ok[1] = ok[1] && r1;
         }
 #pragma unroll
-        for (int v = 0; v < 5; ++v) hbuf[f * HS + v * NQF + q] = h[v];
+        for (int k = 0; k < 2; ++k) {
+            if (k == 1 && p0 + FACE_THREADS >= npairs) break;
+            if (!ok[k]) {
+                flag(err, 0, uint32_t(fid[k]));
+#pragma unroll
+                for (int v = 0; v < 5; ++v) h[k][v] = T(0);
+            }
+#pragma unroll
+            for (int v = 0; v < 5; ++v) hbuf[fid[k] * HS + v * NQF + qv[k]] = h[k][v];
+        }
     }
 }
 
@@ -241,8 +266,9 @@ __global__ void __launch_bounds__(FACE_THREADS, 4) face_flux_kernel(const hodg_m
 //           in flight while the volume integral runs;
 //  per chunk of QC volume points:
 //    phase A: thread (v, e): traces of variable v (coefficients in registers);
-//    phase B: thread (e, q): Euler flux, contravariant flux J^-1 F;
-//    phase C: thread (v, e): volume integral (weighted derivative tables);
+//    phase BC: thread (v, e): primitive state, flux of variable v,
+//              contravariant flux J^-1 F, volume integral (weighted
+//              derivative tables);
 //  gather: thread (v, e): the four face fluxes against the face tables,
 //  then the reference mass solve (FP64), RK combination, dt / norm epilogues.
 // Geometry tiles are field-major ([tile][field][E]) so every smem access in
@@ -329,46 +355,46 @@ __global__ void __launch_bounds__(ETHREADS) elem_stage_kernel(const hodg_mesh_de
             });
         }
         __syncthreads();
-        // phase B
-        for (int p = t; p < nq * E; p += ETHREADS) {
-            const int qq = p / E;
-            const int ee = p - qq * E;
-            if (ee >= ne) continue;
-            T* sl = X + (qq * E + ee) * XS;
-            T U[5];
-#pragma unroll
-            for (int k = 0; k < 5; ++k) U[k] = sl[k];
-            T u, vv, w;
-            const T pr = (U[0] > T(0)) ? prim(U, gam, u, vv, w) : T(-1);
-            if (!(pr > T(0))) {
-                flag(err, 1, uint32_t(e0 + ee));
-#pragma unroll
-                for (int k = 0; k < XS; ++k) sl[k] = T(0);
-                continue;
-            }
-            const T Hs = U[4] + pr;
-            const T F[3][5] = {{U[1], U[1] * u + pr, U[1] * vv, U[1] * w, Hs * u},
-                               {U[2], U[2] * u, U[2] * vv + pr, U[2] * w, Hs * vv},
-                               {U[3], U[3] * u, U[3] * vv, U[3] * w + pr, Hs * w}};
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                const T j0 = T(G[(3 * k) * E + ee]), j1 = T(G[(3 * k + 1) * E + ee]), j2 = T(G[(3 * k + 2) * E + ee]);
-#pragma unroll
-                for (int cc = 0; cc < 5; ++cc) sl[k * 5 + cc] = j0 * F[0][cc] + j1 * F[1][cc] + j2 * F[2][cc];
-            }
-        }
-        __syncthreads();
-        // phase C (volume)
+        // phase B+C: thread (v, e) recomputes the primitive state at each qp
+        // (cheap, saves a barrier and the 15-value flux slots), forms the
+        // physical flux of variable v in x, y, z, maps it to the reference
+        // frame (J^-1 F) and accumulates against the weighted derivatives.
         if (live) {
+            const T j00 = T(G[0 * E + e]), j01 = T(G[1 * E + e]), j02 = T(G[2 * E + e]);
+            const T j10 = T(G[3 * E + e]), j11 = T(G[4 * E + e]), j12 = T(G[5 * E + e]);
+            const T j20 = T(G[6 * E + e]), j21 = T(G[7 * E + e]), j22 = T(G[8 * E + e]);
+            bool bad = false;
             sfor<nq>([&](auto qq) {
                 const T* sl = X + (qq * E + e) * XS;
-                const T fd[3] = {sl[v], sl[5 + v], sl[10 + v]};
+                T U[5];
+#pragma unroll
+                for (int k = 0; k < 5; ++k) U[k] = sl[k];
+                T u, vv, w;
+                const T pr = prim(U, gam, u, vv, w);
+                bad |= !(U[0] > T(0)) || !(pr > T(0));
+                // physical flux of variable v in x, y, z
+                T fx, fy, fz;
+                if (v == 0) {
+                    fx = U[1]; fy = U[2]; fz = U[3];
+                } else if (v == 4) {
+                    const T Hs = U[4] + pr;
+                    fx = Hs * u; fy = Hs * vv; fz = Hs * w;
+                } else {
+                    const T m = U[v];
+                    fx = m * u; fy = m * vv; fz = m * w;
+                    if (v == 1) fx += pr;
+                    if (v == 2) fy += pr;
+                    if (v == 3) fz += pr;
+                }
+                const T fd[3] = {j00 * fx + j01 * fy + j02 * fz, j10 * fx + j11 * fy + j12 * fz,
+                                 j20 * fx + j21 * fy + j22 * fz};
                 sfor<NB>([&](auto i) {
                     sfor<3>([&](auto d) {
                         if constexpr (expt(i, d) > 0) acc[i] += TAB(VD, T, ((q0 + qq) * NB + i) * 3 + d) * fd[d];
                     });
                 });
             });
+            if (bad && v == 0) flag(err, 1, uint32_t(gid));
         }
         __syncthreads();
     });
