@@ -26,8 +26,8 @@ constexpr int FT = FACE_THREADS / (2 * NG);  // faces per CTA (32 for P1-P3)
 constexpr int FBS = NQF * NB + 1;            // padded per-slot stride of the smem trace table
 constexpr int E = (ORDER >= 3) ? 16 : (ORDER == 2 ? 32 : 64);  // elements per CTA
 constexpr int ETHREADS = 5 * E;
-constexpr int XS = 5;                         // smem slot per (element, qp): the 5 traces
-constexpr int QC = (NQV <= 14) ? NQV : 12;  // volume qps per chunk (bounds the X buffer)
+constexpr int XS = 15;                        // smem slot per (element, qp): 5 traces -> 15 contravariant fluxes
+constexpr int QC = (NQV <= 8) ? NQV : (ORDER == 2 ? 7 : 8);  // volume qps per chunk (bounds the X buffer)
 constexpr int NCH = (NQV + QC - 1) / QC;
 
 // padded per-face record of the face flux buffer: 5 x NQF values rounded up
@@ -110,7 +110,8 @@ template <typename T>
 __global__ void __launch_bounds__(FACE_THREADS, 4) face_flux_kernel(const hodg_mesh_desc m,
                                                                     const double* __restrict__ state,
                                                                     T* __restrict__ hbuf,
-                                                                    uint32_t* __restrict__ err) {
+                                                                    uint32_t* __restrict__ err, int64_t f_begin,
+                                                                    int64_t f_end) {
     constexpr int HS = hstride<T>();
     extern __shared__ __align__(16) unsigned char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
@@ -121,8 +122,8 @@ __global__ void __launch_bounds__(FACE_THREADS, 4) face_flux_kernel(const hodg_m
     __shared__ int finf[FT];
 
     const int t = threadIdx.x;
-    const int64_t f0 = int64_t(blockIdx.x) * FT;
-    const int nf = int(min(int64_t(FT), m.n_faces - f0));
+    const int64_t f0 = f_begin + int64_t(blockIdx.x) * FT;
+    const int nf = int(min(int64_t(FT), f_end - f0));
     const int side = t / (FT * NG);
     const int rem = t - side * FT * NG;
     const int lf = rem / NG;
@@ -266,9 +267,8 @@ __global__ void __launch_bounds__(FACE_THREADS, 4) face_flux_kernel(const hodg_m
 //           in flight while the volume integral runs;
 //  per chunk of QC volume points:
 //    phase A: thread (v, e): traces of variable v (coefficients in registers);
-//    phase BC: thread (v, e): primitive state, flux of variable v,
-//              contravariant flux J^-1 F, volume integral (weighted
-//              derivative tables);
+//    phase B: thread (e, q): Euler flux, contravariant flux J^-1 F;
+//    phase C: thread (v, e): volume integral (weighted derivative tables);
 //  gather: thread (v, e): the four face fluxes against the face tables,
 //  then the reference mass solve (FP64), RK combination, dt / norm epilogues.
 // Geometry tiles are field-major ([tile][field][E]) so every smem access in
@@ -355,46 +355,46 @@ __global__ void __launch_bounds__(ETHREADS) elem_stage_kernel(const hodg_mesh_de
             });
         }
         __syncthreads();
-        // phase B+C: thread (v, e) recomputes the primitive state at each qp
-        // (cheap, saves a barrier and the 15-value flux slots), forms the
-        // physical flux of variable v in x, y, z, maps it to the reference
-        // frame (J^-1 F) and accumulates against the weighted derivatives.
+        // phase B
+        for (int p = t; p < nq * E; p += ETHREADS) {
+            const int qq = p / E;
+            const int ee = p - qq * E;
+            if (ee >= ne) continue;
+            T* sl = X + (qq * E + ee) * XS;
+            T U[5];
+#pragma unroll
+            for (int k = 0; k < 5; ++k) U[k] = sl[k];
+            T u, vv, w;
+            const T pr = (U[0] > T(0)) ? prim(U, gam, u, vv, w) : T(-1);
+            if (!(pr > T(0))) {
+                flag(err, 1, uint32_t(e0 + ee));
+#pragma unroll
+                for (int k = 0; k < XS; ++k) sl[k] = T(0);
+                continue;
+            }
+            const T Hs = U[4] + pr;
+            const T F[3][5] = {{U[1], U[1] * u + pr, U[1] * vv, U[1] * w, Hs * u},
+                               {U[2], U[2] * u, U[2] * vv + pr, U[2] * w, Hs * vv},
+                               {U[3], U[3] * u, U[3] * vv, U[3] * w + pr, Hs * w}};
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const T j0 = T(G[(3 * k) * E + ee]), j1 = T(G[(3 * k + 1) * E + ee]), j2 = T(G[(3 * k + 2) * E + ee]);
+#pragma unroll
+                for (int cc = 0; cc < 5; ++cc) sl[k * 5 + cc] = j0 * F[0][cc] + j1 * F[1][cc] + j2 * F[2][cc];
+            }
+        }
+        __syncthreads();
+        // phase C (volume)
         if (live) {
-            const T j00 = T(G[0 * E + e]), j01 = T(G[1 * E + e]), j02 = T(G[2 * E + e]);
-            const T j10 = T(G[3 * E + e]), j11 = T(G[4 * E + e]), j12 = T(G[5 * E + e]);
-            const T j20 = T(G[6 * E + e]), j21 = T(G[7 * E + e]), j22 = T(G[8 * E + e]);
-            bool bad = false;
             sfor<nq>([&](auto qq) {
                 const T* sl = X + (qq * E + e) * XS;
-                T U[5];
-#pragma unroll
-                for (int k = 0; k < 5; ++k) U[k] = sl[k];
-                T u, vv, w;
-                const T pr = prim(U, gam, u, vv, w);
-                bad |= !(U[0] > T(0)) || !(pr > T(0));
-                // physical flux of variable v in x, y, z
-                T fx, fy, fz;
-                if (v == 0) {
-                    fx = U[1]; fy = U[2]; fz = U[3];
-                } else if (v == 4) {
-                    const T Hs = U[4] + pr;
-                    fx = Hs * u; fy = Hs * vv; fz = Hs * w;
-                } else {
-                    const T m = U[v];
-                    fx = m * u; fy = m * vv; fz = m * w;
-                    if (v == 1) fx += pr;
-                    if (v == 2) fy += pr;
-                    if (v == 3) fz += pr;
-                }
-                const T fd[3] = {j00 * fx + j01 * fy + j02 * fz, j10 * fx + j11 * fy + j12 * fz,
-                                 j20 * fx + j21 * fy + j22 * fz};
+                const T fd[3] = {sl[v], sl[5 + v], sl[10 + v]};
                 sfor<NB>([&](auto i) {
                     sfor<3>([&](auto d) {
                         if constexpr (expt(i, d) > 0) acc[i] += TAB(VD, T, ((q0 + qq) * NB + i) * 3 + d) * fd[d];
                     });
                 });
             });
-            if (bad && v == 0) flag(err, 1, uint32_t(gid));
         }
         __syncthreads();
     });
@@ -590,7 +590,8 @@ namespace hodg {
 namespace HODG_CAT(ord, ORDER) {
 
 template <typename T>
-static int launch_face(const hodg_mesh_desc& m, const double* state, void* hbuf, uint32_t* err, cudaStream_t st) {
+static int launch_face(const hodg_mesh_desc& m, const double* state, void* hbuf, uint32_t* err, cudaStream_t st,
+                       int64_t fb, int64_t fe) {
     const size_t sm = face_smem_bytes<T>();
     static bool attr = false;
     if (!attr) {
@@ -599,9 +600,9 @@ static int launch_face(const hodg_mesh_desc& m, const double* state, void* hbuf,
             return HODG_ECUDA;
         attr = true;
     }
-    const int64_t nblk = (m.n_faces + FT - 1) / FT;
+    const int64_t nblk = (fe - fb + FT - 1) / FT;
     if (nblk > 0)
-        face_flux_kernel<T><<<unsigned(nblk), FACE_THREADS, sm, st>>>(m, state, static_cast<T*>(hbuf), err);
+        face_flux_kernel<T><<<unsigned(nblk), FACE_THREADS, sm, st>>>(m, state, static_cast<T*>(hbuf), err, fb, fe);
     return cudaGetLastError() == cudaSuccess ? HODG_OK : HODG_ECUDA;
 }
 
@@ -627,10 +628,10 @@ static int launch_elem(const hodg_mesh_desc& m, const void* hbuf, const hodg_sta
 
 extern "C++" {
 int HODG_CAT(hodg_launch_face_p, ORDER)(const hodg_mesh_desc& m, int prec, const double* state, void* hbuf,
-                                         uint32_t* err, cudaStream_t st) {
+                                         uint32_t* err, cudaStream_t st, int64_t fb, int64_t fe) {
     using namespace hodg::HODG_CAT(ord, ORDER);
-    return prec == HODG_PREC_MIXED ? launch_face<float>(m, state, hbuf, err, st)
-                                   : launch_face<double>(m, state, hbuf, err, st);
+    return prec == HODG_PREC_MIXED ? launch_face<float>(m, state, hbuf, err, st, fb, fe)
+                                   : launch_face<double>(m, state, hbuf, err, st, fb, fe);
 }
 
 int HODG_CAT(hodg_launch_elem_p, ORDER)(const hodg_mesh_desc& m, int prec, const void* hbuf,

@@ -109,7 +109,8 @@ class Discretization:
     (hodg/dg.py:476-534): the C-ABI mesh descriptor over device geometry,
     plus the error word and scratch reused across calls."""
 
-    def __init__(self, mesh: TetMesh, geo: DeviceGeometry, gas: GasModel, bcs: BoundaryConditions, device="cuda"):
+    def __init__(self, mesh: TetMesh, geo: DeviceGeometry, gas: GasModel, bcs: BoundaryConditions, device="cuda",
+                 n_elems: int | None = None):
         if gas.ivis:
             raise NotImplementedError("viscous (BR1) terms are not in the B200 path yet; use ivis=0")
         torch = _torch()
@@ -120,7 +121,10 @@ class Discretization:
         self.nb = geo.n_basis
         self.nqf = geo.n_face_points
         self.rs = int(self.L.hodg_state_row_stride(self.order))
-        self.n = mesh.n_cells
+        # state rows (owned + ghost elements in a partitioned run) vs the
+        # elements the element kernel updates (the owned ones, stored first)
+        self.n_rows = mesh.n_cells
+        self.n = mesh.n_cells if n_elems is None else int(n_elems)
         self.nf = mesh.n_faces
         d = geo.device(self.device)
         self._d = d
@@ -166,8 +170,9 @@ class Discretization:
             self._hbuf[prec] = b
         return b
 
-    def new_state(self):
-        return _torch().zeros((self.n, self.rs), dtype=_torch().float64, device=self.device)
+    def new_state(self, rows=None):
+        return _torch().zeros((self.n_rows if rows is None else rows, self.rs), dtype=_torch().float64,
+                              device=self.device)
 
     # -- basis conversions -------------------------------------------------
     def to_reference(self, coeffs, out=None):
@@ -176,8 +181,8 @@ class Discretization:
         c = torch.as_tensor(coeffs, device=self.device).to(torch.float64)
         if tuple(c.shape) != (self.n, N_VARS, self.nb):
             raise ValueError(f"state shape {tuple(c.shape)} != {(self.n, N_VARS, self.nb)}")
-        src = torch.zeros((self.n, self.rs), dtype=torch.float64, device=self.device)
-        src[:, : N_VARS * self.nb] = c.reshape(self.n, -1)
+        src = self.new_state()
+        src[: self.n, : N_VARS * self.nb] = c.reshape(self.n, -1)
         out = self.new_state() if out is None else out
         _lib.check(self.L.hodg_modal_transform(self.handle, 1, _lib.ptr(src), _lib.ptr(out), _lib.stream_ptr()),
                    "hodg_modal_transform")
@@ -188,7 +193,7 @@ class Discretization:
         out = self.new_state()
         _lib.check(self.L.hodg_modal_transform(self.handle, 0, _lib.ptr(rows), _lib.ptr(out), _lib.stream_ptr()),
                    "hodg_modal_transform")
-        return out[:, : N_VARS * self.nb].reshape(self.n, N_VARS, self.nb)
+        return out[: self.n, : N_VARS * self.nb].reshape(self.n, N_VARS, self.nb)
 
     # -- kernels -----------------------------------------------------------
     def reset_errors(self):
@@ -207,10 +212,12 @@ class Discretization:
         if kind == 3:
             raise AdmissibilityError("inadmissible cell mean", cell=int(idv.value), iteration=iteration)
 
-    def face_flux(self, rows, prec, hbuf=None, stream=None):
+    def face_flux(self, rows, prec, hbuf=None, stream=None, f_begin=0, f_end=None):
         hbuf = self.face_buffer(prec) if hbuf is None else hbuf
-        _lib.check(self.L.hodg_face_flux(self.handle, prec, _lib.ptr(rows), _lib.ptr(hbuf), _lib.ptr(self.err),
-                                         _lib.stream_ptr(stream)), "hodg_face_flux")
+        f_end = self.nf if f_end is None else f_end
+        _lib.check(self.L.hodg_face_flux_range(self.handle, prec, _lib.ptr(rows), _lib.ptr(hbuf), int(f_begin),
+                                               int(f_end), _lib.ptr(self.err), _lib.stream_ptr(stream)),
+                   "hodg_face_flux_range")
         return hbuf
 
     def stage(self, prec, hbuf, args: _lib.StageArgs, stream=None):
@@ -264,7 +271,7 @@ def project_initial(mesh: TetMesh, geo: DeviceGeometry, field, gas: GasModel, de
     ref = np.einsum("iq,nqv->nvi", t.projector, q)  # (n, 5, nb) reference basis
     disc = _get_disc(mesh, geo, gas, BoundaryConditions(Conserved(1.0, 0.0, 0.0, 0.0, 1.0)))
     rows = disc.new_state()
-    rows[:, : N_VARS * t.nb] = torch.from_numpy(ref.reshape(mesh.n_cells, -1)).to(disc.device)
+    rows[: mesh.n_cells, : N_VARS * t.nb] = torch.from_numpy(ref.reshape(mesh.n_cells, -1)).to(disc.device)
     return DofState(disc.from_reference(rows).clone())
 
 
