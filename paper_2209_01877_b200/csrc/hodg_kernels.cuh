@@ -114,7 +114,6 @@ __global__ void __launch_bounds__(FACE_THREADS, 4) face_flux_kernel(const hodg_m
                                                                     int64_t f_end) {
     constexpr int HS = hstride<T>();
     extern __shared__ __align__(16) unsigned char smem[];
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
     T* fbt = reinterpret_cast<T*>(smem + 16);
     double* rows = reinterpret_cast<double*>(smem + align16(16 + 4 * FBS * sizeof(T)));
     T* trs = reinterpret_cast<T*>(rows);  // aliases rows after phase 1
@@ -129,6 +128,7 @@ __global__ void __launch_bounds__(FACE_THREADS, 4) face_flux_kernel(const hodg_m
     const int lf = rem / NG;
     const int g = rem - lf * NG;
 
+    __shared__ int64_t rowelem[2 * FT];
     int64_t elem = -1;
     int slot = 0;
     if (lf < nf) {
@@ -144,23 +144,25 @@ __global__ void __launch_bounds__(FACE_THREADS, 4) face_flux_kernel(const hodg_m
             fn[lf][2] = nn.z;
         }
     }
-    if (t == 0) {
-        mbar_init(bar, FACE_THREADS);
-        mbar_fence_init();
-    }
+    if (g == 0) rowelem[side * FT + lf] = elem;
+    const T* fbg = sizeof(T) == 8 ? reinterpret_cast<const T*>(FBG_D) : reinterpret_cast<const T*>(FBG_F);
     for (int k = t; k < 4 * NQF * NB; k += FACE_THREADS) {
         const int s = k / (NQF * NB);
-        fbt[s * FBS + (k - s * NQF * NB)] = TAB(FB, T, k);
+        fbt[s * FBS + (k - s * NQF * NB)] = fbg[k];
     }
     __syncthreads();
-    double* myrow = rows + size_t(side * FT + lf) * RS;
-    if (g == 0 && elem >= 0) {
-        mbar_arrive_expect_tx(bar, RS * 8);
-        bulk_g2s(myrow, state + elem * RS, RS * 8, bar);
-    } else {
-        mbar_arrive(bar);
+    // gather both sides' state rows: consecutive threads copy consecutive
+    // 16-byte pieces of a row (coalesced, asynchronous)
+    constexpr int CPR = RS / 2;  // 16-byte pieces per row
+    for (int k = t; k < 2 * FT * CPR; k += FACE_THREADS) {
+        const int r = k / CPR;
+        const int64_t el = rowelem[r];
+        if (el >= 0) cp_async16(rows + size_t(r) * RS + 2 * (k - r * CPR), state + el * RS + 2 * (k - r * CPR));
     }
-    mbar_wait(bar, 0);
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+    double* myrow = rows + size_t(side * FT + lf) * RS;
 
     // phase 1: traces of this side at qps [g*QPT, g*QPT + QPT)
     T tr[QPT][5];
@@ -297,7 +299,6 @@ __global__ void __launch_bounds__(ETHREADS) elem_stage_kernel(const hodg_mesh_de
         if (a.dt_reset && blockIdx.x == 0) *a.dt_reset = 0x7FF0000000000000ull;
         blk_dt = 0x7FF0000000000000ull;
         mbar_init(bar, 1);
-        mbar_init(bar + 1, 4 * E);
         mbar_fence_init();
         const uint32_t bs = uint32_t(ne) * RS * 8;
         mbar_arrive_expect_tx(bar, bs + 16 * E * 8 + 4 * E * 4);
@@ -310,16 +311,21 @@ __global__ void __launch_bounds__(ETHREADS) elem_stage_kernel(const hodg_mesh_de
 
     const int v = t / E;
     const int e = t - v * E;
-    // face flux records: thread (s, e) for t < 4E fetches face FI[s][e]
-    if (t < 4 * E) {
-        const int ee = t % E;
-        if (ee < ne) {
-            const int64_t f = FI[t];
-            mbar_arrive_expect_tx(bar + 1, HS * sizeof(T));
-            bulk_g2s(HT + size_t(t) * HSS, hbuf + f * HS, HS * sizeof(T), bar + 1);
-        } else {
-            mbar_arrive(bar + 1);
+    // face flux records of the tile's 4E (element, face) slots: 16-byte
+    // async copies, consecutive threads on consecutive pieces of a record;
+    // in flight while the volume integral runs
+    {
+        constexpr int CPR = HS * int(sizeof(T)) / 16;
+        for (int k = t; k < 4 * E * CPR; k += ETHREADS) {
+            const int r = k / CPR;
+            const int piece = k - r * CPR;
+            if (r % E < ne) {
+                const int64_t f = FI[r];
+                cp_async16(reinterpret_cast<char*>(HT + size_t(r) * HSS) + 16 * piece,
+                           reinterpret_cast<const char*>(hbuf + f * HS) + 16 * piece);
+            }
         }
+        cp_async_commit();
     }
 
     const int64_t gid = e0 + e;
@@ -400,7 +406,8 @@ __global__ void __launch_bounds__(ETHREADS) elem_stage_kernel(const hodg_mesh_de
     });
 
     // face gather, mass solve, RK update
-    mbar_wait(bar + 1, 0);
+    cp_async_wait_all();
+    __syncthreads();
     if (live) {
         double accd[NB];
 #pragma unroll

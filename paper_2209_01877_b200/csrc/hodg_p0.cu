@@ -12,6 +12,8 @@
 #define FB_F FB_P0_f
 #define FG_D FG_P0_d
 #define FG_F FG_P0_f
+#define FBG_D FBG_P0_d
+#define FBG_F FBG_P0_f
 #define MINV_T MINV_P0
 #define MEAN_T MEAN_P0
 #include "hodg_kernels.cuh"

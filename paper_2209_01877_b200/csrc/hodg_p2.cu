@@ -12,6 +12,8 @@
 #define FB_F FB_P2_f
 #define FG_D FG_P2_d
 #define FG_F FG_P2_f
+#define FBG_D FBG_P2_d
+#define FBG_F FBG_P2_f
 #define MINV_T MINV_P2
 #define MEAN_T MEAN_P2
 #include "hodg_kernels.cuh"
