@@ -19,7 +19,7 @@ namespace hodg {
 namespace HODG_CAT(ord, ORDER) {
 
 constexpr int RS = (5 * NB + 1) & ~1;        // state row stride (doubles)
-constexpr int NG = (NQF > 1) ? 2 : 1;        // face qp groups per side thread
+constexpr int NG = 2;                        // face qp groups per side thread
 constexpr int QPT = (NQF + NG - 1) / NG;     // face qps per phase-1 thread
 constexpr int FACE_THREADS = 128;
 constexpr int FT = FACE_THREADS / (2 * NG);  // faces per CTA (32 for P1-P3)
@@ -151,15 +151,22 @@ __global__ void __launch_bounds__(FACE_THREADS, 4) face_flux_kernel(const hodg_m
         fbt[s * FBS + (k - s * NQF * NB)] = fbg[k];
     }
     __syncthreads();
-    // gather both sides' state rows: consecutive threads copy consecutive
-    // 16-byte pieces of a row (coalesced, asynchronous)
-    constexpr int CPR = RS / 2;  // 16-byte pieces per row
-    for (int k = t; k < 2 * FT * CPR; k += FACE_THREADS) {
-        const int r = k / CPR;
+    // gather both sides' state rows: a thread pair per row, alternating
+    // 16-byte pieces (each pair fills whole 32-byte sectors), asynchronous
+    {
+        constexpr int CPR = RS / 2;  // 16-byte pieces per row
+        static_assert(FACE_THREADS == 4 * FT, "one thread pair per row");
+        const int r = t >> 1;
+        const int h = t & 1;
         const int64_t el = rowelem[r];
-        if (el >= 0) cp_async16(rows + size_t(r) * RS + 2 * (k - r * CPR), state + el * RS + 2 * (k - r * CPR));
+        if (el >= 0) {
+            const double* src = state + el * RS;
+            double* dst = rows + size_t(r) * RS;
+#pragma unroll
+            for (int k = h; k < CPR; k += 2) cp_async16(dst + 2 * k, src + 2 * k);
+        }
+        cp_async_commit();
     }
-    cp_async_commit();
     cp_async_wait_all();
     __syncthreads();
     double* myrow = rows + size_t(side * FT + lf) * RS;
@@ -315,14 +322,13 @@ __global__ void __launch_bounds__(ETHREADS) elem_stage_kernel(const hodg_mesh_de
     // async copies, consecutive threads on consecutive pieces of a record;
     // in flight while the volume integral runs
     {
-        constexpr int CPR = HS * int(sizeof(T)) / 16;
-        for (int k = t; k < 4 * E * CPR; k += ETHREADS) {
-            const int r = k / CPR;
-            const int piece = k - r * CPR;
+        constexpr int CPR = HS * int(sizeof(T)) / 16;  // 16-byte pieces per record
+        for (int r = t; r < 4 * E; r += ETHREADS) {
             if (r % E < ne) {
-                const int64_t f = FI[r];
-                cp_async16(reinterpret_cast<char*>(HT + size_t(r) * HSS) + 16 * piece,
-                           reinterpret_cast<const char*>(hbuf + f * HS) + 16 * piece);
+                const char* src = reinterpret_cast<const char*>(hbuf + int64_t(FI[r]) * HS);
+                char* dst = reinterpret_cast<char*>(HT + size_t(r) * HSS);
+#pragma unroll
+                for (int k = 0; k < CPR; ++k) cp_async16(dst + 16 * k, src + 16 * k);
             }
         }
         cp_async_commit();
