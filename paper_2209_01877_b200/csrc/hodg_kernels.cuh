@@ -19,7 +19,7 @@ namespace hodg {
 namespace HODG_CAT(ord, ORDER) {
 
 constexpr int RS = (5 * NB + 1) & ~1;        // state row stride (doubles)
-constexpr int NG = 2;                        // face qp groups per side thread
+constexpr int NG = (NQF > 1) ? 2 : 1;        // face qp groups per side thread
 constexpr int QPT = (NQF + NG - 1) / NG;     // face qps per phase-1 thread
 constexpr int FACE_THREADS = 128;
 constexpr int FT = FACE_THREADS / (2 * NG);  // faces per CTA (32 for P1-P3)
@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(FACE_THREADS, 4) face_flux_kernel(const hodg_m
                                                                     int64_t f_end) {
     constexpr int HS = hstride<T>();
     extern __shared__ __align__(16) unsigned char smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
     T* fbt = reinterpret_cast<T*>(smem + 16);
     double* rows = reinterpret_cast<double*>(smem + align16(16 + 4 * FBS * sizeof(T)));
     T* trs = reinterpret_cast<T*>(rows);  // aliases rows after phase 1
@@ -128,7 +129,6 @@ __global__ void __launch_bounds__(FACE_THREADS, 4) face_flux_kernel(const hodg_m
     const int lf = rem / NG;
     const int g = rem - lf * NG;
 
-    __shared__ int64_t rowelem[2 * FT];
     int64_t elem = -1;
     int slot = 0;
     if (lf < nf) {
@@ -144,32 +144,23 @@ __global__ void __launch_bounds__(FACE_THREADS, 4) face_flux_kernel(const hodg_m
             fn[lf][2] = nn.z;
         }
     }
-    if (g == 0) rowelem[side * FT + lf] = elem;
-    const T* fbg = sizeof(T) == 8 ? reinterpret_cast<const T*>(FBG_D) : reinterpret_cast<const T*>(FBG_F);
+    if (t == 0) {
+        mbar_init(bar, FACE_THREADS);
+        mbar_fence_init();
+    }
     for (int k = t; k < 4 * NQF * NB; k += FACE_THREADS) {
         const int s = k / (NQF * NB);
-        fbt[s * FBS + (k - s * NQF * NB)] = fbg[k];
+        fbt[s * FBS + (k - s * NQF * NB)] = TAB(FB, T, k);
     }
-    __syncthreads();
-    // gather both sides' state rows: a thread pair per row, alternating
-    // 16-byte pieces (each pair fills whole 32-byte sectors), asynchronous
-    {
-        constexpr int CPR = RS / 2;  // 16-byte pieces per row
-        static_assert(FACE_THREADS == 4 * FT, "one thread pair per row");
-        const int r = t >> 1;
-        const int h = t & 1;
-        const int64_t el = rowelem[r];
-        if (el >= 0) {
-            const double* src = state + el * RS;
-            double* dst = rows + size_t(r) * RS;
-#pragma unroll
-            for (int k = h; k < CPR; k += 2) cp_async16(dst + 2 * k, src + 2 * k);
-        }
-        cp_async_commit();
-    }
-    cp_async_wait_all();
     __syncthreads();
     double* myrow = rows + size_t(side * FT + lf) * RS;
+    if (g == 0 && elem >= 0) {
+        mbar_arrive_expect_tx(bar, RS * 8);
+        bulk_g2s(myrow, state + elem * RS, RS * 8, bar);
+    } else {
+        mbar_arrive(bar);
+    }
+    mbar_wait(bar, 0);
 
     // phase 1: traces of this side at qps [g*QPT, g*QPT + QPT)
     T tr[QPT][5];
@@ -306,6 +297,7 @@ __global__ void __launch_bounds__(ETHREADS) elem_stage_kernel(const hodg_mesh_de
         if (a.dt_reset && blockIdx.x == 0) *a.dt_reset = 0x7FF0000000000000ull;
         blk_dt = 0x7FF0000000000000ull;
         mbar_init(bar, 1);
+        mbar_init(bar + 1, 4 * E);
         mbar_fence_init();
         const uint32_t bs = uint32_t(ne) * RS * 8;
         mbar_arrive_expect_tx(bar, bs + 16 * E * 8 + 4 * E * 4);
@@ -318,20 +310,16 @@ __global__ void __launch_bounds__(ETHREADS) elem_stage_kernel(const hodg_mesh_de
 
     const int v = t / E;
     const int e = t - v * E;
-    // face flux records of the tile's 4E (element, face) slots: 16-byte
-    // async copies, consecutive threads on consecutive pieces of a record;
-    // in flight while the volume integral runs
-    {
-        constexpr int CPR = HS * int(sizeof(T)) / 16;  // 16-byte pieces per record
-        for (int r = t; r < 4 * E; r += ETHREADS) {
-            if (r % E < ne) {
-                const char* src = reinterpret_cast<const char*>(hbuf + int64_t(FI[r]) * HS);
-                char* dst = reinterpret_cast<char*>(HT + size_t(r) * HSS);
-#pragma unroll
-                for (int k = 0; k < CPR; ++k) cp_async16(dst + 16 * k, src + 16 * k);
-            }
+    // face flux records: thread (s, e) for t < 4E fetches face FI[s][e]
+    if (t < 4 * E) {
+        const int ee = t % E;
+        if (ee < ne) {
+            const int64_t f = FI[t];
+            mbar_arrive_expect_tx(bar + 1, HS * sizeof(T));
+            bulk_g2s(HT + size_t(t) * HSS, hbuf + f * HS, HS * sizeof(T), bar + 1);
+        } else {
+            mbar_arrive(bar + 1);
         }
-        cp_async_commit();
     }
 
     const int64_t gid = e0 + e;
@@ -412,8 +400,7 @@ __global__ void __launch_bounds__(ETHREADS) elem_stage_kernel(const hodg_mesh_de
     });
 
     // face gather, mass solve, RK update
-    cp_async_wait_all();
-    __syncthreads();
+    mbar_wait(bar + 1, 0);
     if (live) {
         double accd[NB];
 #pragma unroll
