@@ -148,9 +148,12 @@ __global__ void __launch_bounds__(FACE_THREADS, 4) face_flux_kernel(const hodg_m
         mbar_init(bar, FACE_THREADS);
         mbar_fence_init();
     }
+    // stage the face trace table from its global-memory copy (coalesced; a
+    // runtime-indexed __constant__ read would serialise across the warp)
+    const T* fbg = sizeof(T) == 8 ? reinterpret_cast<const T*>(FBG_D) : reinterpret_cast<const T*>(FBG_F);
     for (int k = t; k < 4 * NQF * NB; k += FACE_THREADS) {
         const int s = k / (NQF * NB);
-        fbt[s * FBS + (k - s * NQF * NB)] = TAB(FB, T, k);
+        fbt[s * FBS + (k - s * NQF * NB)] = fbg[k];
     }
     __syncthreads();
     double* myrow = rows + size_t(side * FT + lf) * RS;
