@@ -58,10 +58,10 @@ for r in rr[2:]:
     out.append("\nTop stall reasons (warps per issue): " + ", ".join(
         f"{s.replace('smsp__average_warps_issue_stalled_', '').replace('_per_issue_active.ratio', '')} {float(v):.2f}"
         for s, v in stalls) + "\n")
-    rb = float(r[h.index("dram__bytes_read.sum")].replace(",", ""))
-    wb = float(r[h.index("dram__bytes_write.sum")].replace(",", ""))
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[u[h.index("dram__bytes_read.sum")]]
-    traffic["face" if "face" in name else "elem"] = (rb + wb) * scale
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    rb = float(r[h.index("dram__bytes_read.sum")].replace(",", "")) * scale[u[h.index("dram__bytes_read.sum")]]
+    wb = float(r[h.index("dram__bytes_write.sum")].replace(",", "")) * scale[u[h.index("dram__bytes_write.sum")]]
+    traffic["face" if "face" in name else "elem"] = rb + wb
 open(os.path.join(root, "profiles", f"{tag}_summary.md"), "w").write("\n".join(out) + "\n")
 tj = os.path.join(root, "profiles", "traffic.json")
 d = json.load(open(tj)) if os.path.exists(tj) else {}
