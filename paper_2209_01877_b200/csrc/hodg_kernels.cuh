@@ -290,15 +290,12 @@ __global__ void __launch_bounds__(ETHREADS) elem_stage_kernel(const hodg_mesh_de
     T* HT = reinterpret_cast<T*>(smem + L::htile);
     double* S = reinterpret_cast<double*>(smem + L::sx);  // state tile, later the output tile
     T* X = reinterpret_cast<T*>(smem + L::sx);            // per-chunk trace / flux slots
-    __shared__ unsigned long long blk_dt;
-
     const int t = threadIdx.x;
     const int64_t tile = blockIdx.x;
     const int64_t e0 = tile * E;
     const int ne = int(min(int64_t(E), m.n_elems - e0));
     if (t == 0) {
         if (a.dt_reset && blockIdx.x == 0) *a.dt_reset = 0x7FF0000000000000ull;
-        blk_dt = 0x7FF0000000000000ull;
         mbar_init(bar, 1);
         mbar_init(bar + 1, 4 * E);
         mbar_fence_init();
@@ -459,34 +456,59 @@ __global__ void __launch_bounds__(ETHREADS) elem_stage_kernel(const hodg_mesh_de
     fence_proxy_async();
     __syncthreads();
     if (t == 0 && a.combine >= 0 && ne > 0) bulk_s2g(a.out + e0 * RS, S, uint32_t(ne) * RS * 8);
-    if (a.norm_partial && t < 5) {
-        double s = 0.0;
-        for (int k = 0; k < ne; ++k) s += RED[t * E + k];
-        a.norm_partial[int64_t(blockIdx.x) * 5 + t] = s;
-    }
-    if (a.combine >= 0 && (a.dt_next || a.dt_vec_out) && t < ne) {
-        // CFL dt of the new cell mean (hodg/timestepping.py:121-134), 3D
-        const double m0 = RED[5 * E + t], m1 = RED[6 * E + t], m2 = RED[7 * E + t], m3 = RED[8 * E + t],
-                     m4 = RED[9 * E + t];
-        double dt = 0.0;
-        if (!(m0 > 0.0)) {
-            flag(err, 2, uint32_t(e0 + t));
-        } else {
-            const double u = m1 / m0, vv = m2 / m0, w = m3 / m0;
-            const double p = (m.gamma - 1.0) * (m4 - 0.5 * m0 * (u * u + vv * vv + w * w));
-            if (!(p > 0.0)) {
-                flag(err, 2, uint32_t(e0 + t));
-            } else {
-                const double speed = sqrt(u * u + vv * vv + w * w) + sqrt(m.gamma * p / m0);
-                dt = a.cfl * G[13 * E + t] / ((2.0 * ORDER + 1.0) * speed);
-                if (a.dt_next) atomicMin(&blk_dt, static_cast<unsigned long long>(__double_as_longlong(dt)));
-            }
+    // epilogues without a trailing barrier: fixed-order shuffle trees
+    const int lane = t & 31;
+    if (a.norm_partial) {
+        // partial sum over the tile of vol * res_0^2 per variable; warp w
+        // holds variable (32 w) / E (E >= 32) or two variables (E == 16)
+        constexpr int W = E < 32 ? E : 32;
+        double x = (live) ? RED[v * E + e] : 0.0;
+#pragma unroll
+        for (int o = W / 2; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if (E <= 32) {
+            if ((lane % W) == 0) a.norm_partial[int64_t(blockIdx.x) * 5 + v] = x;
+        } else {  // E == 64: two warps per variable, combined in a fixed order
+            __shared__ double half2[10];
+            if (lane == 0) half2[(t / 32)] = x;
+            __syncthreads();
+            if (t < 5) a.norm_partial[int64_t(blockIdx.x) * 5 + t] = half2[2 * t] + half2[2 * t + 1];
         }
-        if (a.dt_vec_out) a.dt_vec_out[e0 + t] = dt;
     }
-    if (a.dt_next) {
-        __syncthreads();
-        if (t == 0) atomicMin(a.dt_next, blk_dt);
+    if (a.combine >= 0 && (a.dt_next || a.dt_vec_out) && v == 0) {
+        // CFL dt of the new cell mean (hodg/timestepping.py:121-134), 3D;
+        // threads (0, e) of warp(s) 0 (.. E/32), no other warp waits
+        double dt = 0.0;
+        bool okdt = false;
+        if (live) {
+            const double m0 = RED[5 * E + e], m1 = RED[6 * E + e], m2 = RED[7 * E + e], m3 = RED[8 * E + e],
+                         m4 = RED[9 * E + e];
+            if (!(m0 > 0.0)) {
+                flag(err, 2, uint32_t(gid));
+            } else {
+                const double ri = 1.0 / m0;
+                const double u = m1 * ri, vv = m2 * ri, w = m3 * ri;
+                const double p = (m.gamma - 1.0) * (m4 - 0.5 * m0 * (u * u + vv * vv + w * w));
+                if (!(p > 0.0)) {
+                    flag(err, 2, uint32_t(gid));
+                } else {
+                    const double speed = sqrt(u * u + vv * vv + w * w) + sqrt(m.gamma * p * ri);
+                    dt = a.cfl * G[13 * E + e] / ((2.0 * ORDER + 1.0) * speed);
+                    okdt = true;
+                }
+            }
+            if (a.dt_vec_out) a.dt_vec_out[gid] = dt;
+        }
+        if (a.dt_next) {
+            unsigned long long bits = okdt ? static_cast<unsigned long long>(__double_as_longlong(dt))
+                                           : 0x7FF0000000000000ull;
+            constexpr int W = E < 32 ? E : 32;
+#pragma unroll
+            for (int o = W / 2; o > 0; o >>= 1) {
+                const unsigned long long other = __shfl_xor_sync(0xffffffffu, bits, o);
+                bits = other < bits ? other : bits;
+            }
+            if ((lane % W) == 0) atomicMin(a.dt_next, bits);
+        }
     }
     if (t == 0 && a.combine >= 0 && ne > 0) bulk_wait_read();
 }
