@@ -502,9 +502,10 @@ __global__ void __launch_bounds__(ETHREADS) elem_stage_kernel(const hodg_mesh_de
             unsigned long long bits = okdt ? static_cast<unsigned long long>(__double_as_longlong(dt))
                                            : 0x7FF0000000000000ull;
             constexpr int W = E < 32 ? E : 32;
+            constexpr unsigned mask = E < 32 ? ((1u << E) - 1u) : 0xffffffffu;  // lanes with v == 0
 #pragma unroll
             for (int o = W / 2; o > 0; o >>= 1) {
-                const unsigned long long other = __shfl_xor_sync(0xffffffffu, bits, o);
+                const unsigned long long other = __shfl_xor_sync(mask, bits, o);
                 bits = other < bits ? other : bits;
             }
             if ((lane % W) == 0) atomicMin(a.dt_next, bits);
