@@ -75,7 +75,7 @@ __host__ __device__ constexpr int expt(int i, int d) {
 template <typename T>
 __host__ __device__ constexpr size_t face_smem_bytes() {
     return align16(16 + 4 * FBS * sizeof(T)) +
-           align16(cmax(size_t(2 * FT) * RS * sizeof(double), size_t(2 * FT) * NQF * 5 * sizeof(T)));
+           2 * align16(cmax(size_t(2 * FT) * RS * sizeof(double), size_t(2 * FT) * NQF * 5 * sizeof(T)));
 }
 
 // element kernel shared memory carve-up
@@ -114,38 +114,24 @@ __global__ void __launch_bounds__(FACE_THREADS, 4) face_flux_kernel(const hodg_m
                                                                     int64_t f_end) {
     constexpr int HS = hstride<T>();
     extern __shared__ __align__(16) unsigned char smem[];
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);  // one per buffer
     T* fbt = reinterpret_cast<T*>(smem + 16);
-    double* rows = reinterpret_cast<double*>(smem + align16(16 + 4 * FBS * sizeof(T)));
-    T* trs = reinterpret_cast<T*>(rows);  // aliases rows after phase 1
-    __shared__ double fn[FT][3];
-    __shared__ int finf[FT];
+    double* rows0 = reinterpret_cast<double*>(smem + align16(16 + 4 * FBS * sizeof(T)));
+    constexpr size_t BUF = align16(cmax(size_t(2 * FT) * RS * sizeof(double), size_t(2 * FT) * NQF * 5 * sizeof(T))) /
+                           sizeof(double);
+    __shared__ double fn[2][FT][3];
+    __shared__ int finf[2][FT];
 
     const int t = threadIdx.x;
-    const int64_t f0 = f_begin + int64_t(blockIdx.x) * FT;
-    const int nf = int(min(int64_t(FT), f_end - f0));
     const int side = t / (FT * NG);
     const int rem = t - side * FT * NG;
     const int lf = rem / NG;
     const int g = rem - lf * NG;
+    const int64_t ntiles = (f_end - f_begin + FT - 1) / FT;
 
-    int64_t elem = -1;
-    int slot = 0;
-    if (lf < nf) {
-        elem = m.fcells[2 * (f0 + lf) + side];
-        const int info = m.finfo[f0 + lf];
-        slot = side == 0 ? (info & 3) : ((info >> 2) & 3);
-        if (side == 0 && g == 0) {
-            // per-face data for phase 2: bc code and a right-side flag, normal
-            finf[lf] = ((info >> 4) & 15) | (m.fcells[2 * (f0 + lf) + 1] >= 0 ? 0x100 : 0);
-            const double4 nn = reinterpret_cast<const double4*>(m.fnrm)[f0 + lf];
-            fn[lf][0] = nn.x;
-            fn[lf][1] = nn.y;
-            fn[lf][2] = nn.z;
-        }
-    }
     if (t == 0) {
         mbar_init(bar, FACE_THREADS);
+        mbar_init(bar + 1, FACE_THREADS);
         mbar_fence_init();
     }
     // stage the face trace table from its global-memory copy (coalesced; a
@@ -155,109 +141,157 @@ __global__ void __launch_bounds__(FACE_THREADS, 4) face_flux_kernel(const hodg_m
         const int s = k / (NQF * NB);
         fbt[s * FBS + (k - s * NQF * NB)] = fbg[k];
     }
-    __syncthreads();
-    double* myrow = rows + size_t(side * FT + lf) * RS;
-    if (g == 0 && elem >= 0) {
-        mbar_arrive_expect_tx(bar, RS * 8);
-        bulk_g2s(myrow, state + elem * RS, RS * 8, bar);
-    } else {
-        mbar_arrive(bar);
-    }
-    mbar_wait(bar, 0);
 
-    // phase 1: traces of this side at qps [g*QPT, g*QPT + QPT)
-    T tr[QPT][5];
+    // per-tile metadata of this thread's (face, side): element, slot, and
+    // (side 0, group 0 threads) the face's bc / right flag / normal
+    struct Meta {
+        int64_t elem;
+        int slot;
+        int finf;
+        double4 nrm;
+    };
+    auto load_meta = [&](int64_t tile) {
+        Meta mt{-1, 0, 0, make_double4(0, 0, 0, 0)};
+        const int64_t f0 = f_begin + tile * FT;
+        if (tile < ntiles && f0 + lf < f_end) {
+            const int64_t f = f0 + lf;
+            mt.elem = m.fcells[2 * f + side];
+            const int info = m.finfo[f];
+            mt.slot = side == 0 ? (info & 3) : ((info >> 2) & 3);
+            if (side == 0 && g == 0) {
+                mt.finf = ((info >> 4) & 15) | (m.fcells[2 * f + 1] >= 0 ? 0x100 : 0);
+                mt.nrm = reinterpret_cast<const double4*>(m.fnrm)[f];
+            }
+        }
+        return mt;
+    };
+    auto publish = [&](const Meta& mt, int buf) {
+        if (side == 0 && g == 0) {
+            finf[buf][lf] = mt.finf;
+            fn[buf][lf][0] = mt.nrm.x;
+            fn[buf][lf][1] = mt.nrm.y;
+            fn[buf][lf][2] = mt.nrm.z;
+        }
+        double* row = rows0 + buf * BUF + size_t(side * FT + lf) * RS;
+        if (g == 0 && mt.elem >= 0) {
+            mbar_arrive_expect_tx(bar + buf, RS * 8);
+            bulk_g2s(row, state + mt.elem * RS, RS * 8, bar + buf);
+        } else {
+            mbar_arrive(bar + buf);
+        }
+    };
+
+    int64_t tile = blockIdx.x;
+    Meta cur = load_meta(tile);
+    __syncthreads();  // barrier init visible
+    if (tile < ntiles) publish(cur, 0);
+    const T gam = T(m.gamma);
+    for (int it = 0; tile < ntiles; tile += gridDim.x, ++it) {
+        const int buf = it & 1;
+        const int64_t f0 = f_begin + tile * FT;
+        const int nf = int(min(int64_t(FT), f_end - f0));
+        const Meta nxt = load_meta(tile + gridDim.x);  // in flight during this tile
+        mbar_wait(bar + buf, (it >> 1) & 1);
+
+        // phase 1: traces of this side at qps [g*QPT, g*QPT + QPT)
+        const double* myrow = rows0 + buf * BUF + size_t(side * FT + lf) * RS;
+        T tr[QPT][5];
 #pragma unroll
-    for (int qq = 0; qq < QPT; ++qq)
+        for (int qq = 0; qq < QPT; ++qq)
 #pragma unroll
-        for (int v = 0; v < 5; ++v) tr[qq][v] = T(0);
-    if (elem >= 0) {
-        const T* fb = fbt + slot * FBS + g * QPT * NB;
+            for (int v = 0; v < 5; ++v) tr[qq][v] = T(0);
+        if (cur.elem >= 0) {
+            const T* fb = fbt + cur.slot * FBS;
 #pragma unroll
-        for (int i = 0; i < NB; ++i) {
-            T c[5];
+            for (int i = 0; i < NB; ++i) {
+                T c[5];
 #pragma unroll
-            for (int v = 0; v < 5; ++v) c[v] = T(myrow[v * NB + i]);
+                for (int v = 0; v < 5; ++v) c[v] = T(myrow[v * NB + i]);
+#pragma unroll
+                for (int qq = 0; qq < QPT; ++qq) {
+                    const int q = g * QPT + qq;
+                    if (NG * QPT == NQF || q < NQF) {
+                        const T b = fb[q * NB + i];
+#pragma unroll
+                        for (int v = 0; v < 5; ++v) tr[qq][v] += b * c[v];
+                    }
+                }
+            }
+        }
+        __syncthreads();  // rows[buf] consumed; previous tile's phase 2 done everywhere
+        T* trs = reinterpret_cast<T*>(rows0 + buf * BUF);
+        if (lf < nf) {
 #pragma unroll
             for (int qq = 0; qq < QPT; ++qq) {
-                if (NG * QPT == NQF || g * QPT + qq < NQF) {
-                    const T b = fb[qq * NB + i];
+                const int q = g * QPT + qq;
+                if (NG * QPT == NQF || q < NQF) {
 #pragma unroll
-                    for (int v = 0; v < 5; ++v) tr[qq][v] += b * c[v];
+                    for (int v = 0; v < 5; ++v) trs[(size_t(side * FT + lf) * NQF + q) * 5 + v] = tr[qq][v];
                 }
             }
         }
-    }
-    __syncthreads();  // every row consumed; reuse the region for traces
-    if (lf < nf) {
-#pragma unroll
-        for (int qq = 0; qq < QPT; ++qq) {
-            const int q = g * QPT + qq;
-            if (NG * QPT == NQF || q < NQF) {
-#pragma unroll
-                for (int v = 0; v < 5; ++v) trs[(size_t(side * FT + lf) * NQF + q) * 5 + v] = tr[qq][v];
-            }
-        }
-    }
-    __syncthreads();
+        // next tile: its rows stream into the other buffer during phase 2
+        if (tile + gridDim.x < ntiles) publish(nxt, buf ^ 1);
+        __syncthreads();
 
-    // phase 2: Riemann flux at each (face, qp); two pairs per thread per
-    // iteration so their (straight-line) Roe evaluations interleave
-    const T gam = T(m.gamma);
-    const int npairs = nf * NQF;
-    for (int p0 = t; p0 < npairs; p0 += 2 * FACE_THREADS) {
-        T qL[2][5], qR[2][5], h[2][5], n[2][3];
-        bool ok[2];
-        int64_t fid[2];
-        int qv[2];
+        // phase 2: Riemann flux at each (face, qp); two pairs per thread per
+        // iteration so their (straight-line) Roe evaluations interleave
+        const int npairs = nf * NQF;
+        for (int p0 = t; p0 < npairs; p0 += 2 * FACE_THREADS) {
+            T qL[2][5], qR[2][5], h[2][5], n[2][3];
+            bool ok[2];
+            int64_t fid[2];
+            int qv[2];
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            const int p = min(p0 + k * FACE_THREADS, npairs - 1);
-            const int lfp = p / NQF;
-            const int q = p - lfp * NQF;
-            fid[k] = f0 + lfp;
-            qv[k] = q;
-            const int info = finf[lfp];
+            for (int k = 0; k < 2; ++k) {
+                const int p = min(p0 + k * FACE_THREADS, npairs - 1);
+                const int lfp = p / NQF;
+                const int q = p - lfp * NQF;
+                fid[k] = f0 + lfp;
+                qv[k] = q;
+                const int info = finf[buf][lfp];
 #pragma unroll
-            for (int d = 0; d < 3; ++d) n[k][d] = T(fn[lfp][d]);
+                for (int d = 0; d < 3; ++d) n[k][d] = T(fn[buf][lfp][d]);
 #pragma unroll
-            for (int v = 0; v < 5; ++v) qL[k][v] = trs[(size_t(lfp) * NQF + q) * 5 + v];
-            ok[k] = true;
-            if (info & 0x100) {
+                for (int v = 0; v < 5; ++v) qL[k][v] = trs[(size_t(lfp) * NQF + q) * 5 + v];
+                ok[k] = true;
+                if (info & 0x100) {
 #pragma unroll
-                for (int v = 0; v < 5; ++v) qR[k][v] = trs[(size_t(FT + lfp) * NQF + q) * 5 + v];
-            } else {
-                T u, vv, w;
-                if (!(qL[k][0] > T(0)) || !(prim(qL[k], gam, u, vv, w) > T(0))) {
-                    ok[k] = false;
-#pragma unroll
-                    for (int v = 0; v < 5; ++v) qR[k][v] = qL[k][v];
+                    for (int v = 0; v < 5; ++v) qR[k][v] = trs[(size_t(FT + lfp) * NQF + q) * 5 + v];
                 } else {
-                    const T qf[5] = {T(m.qinf[0]), T(m.qinf[1]), T(m.qinf[2]), T(m.qinf[3]), T(m.qinf[4])};
-                    bstate(info & 15, qL[k], n[k], qf, gam, qR[k]);
+                    T u, vv, w;
+                    if (!(qL[k][0] > T(0)) || !(prim(qL[k], gam, u, vv, w) > T(0))) {
+                        ok[k] = false;
+#pragma unroll
+                        for (int v = 0; v < 5; ++v) qR[k][v] = qL[k][v];
+                    } else {
+                        const T qf[5] = {T(m.qinf[0]), T(m.qinf[1]), T(m.qinf[2]), T(m.qinf[3]), T(m.qinf[4])};
+                        bstate(info & 15, qL[k], n[k], qf, gam, qR[k]);
+                    }
                 }
             }
-        }
-        if (m.flux_kind == HODG_FLUX_LLF) {
+            if (m.flux_kind == HODG_FLUX_LLF) {
 #pragma unroll
-            for (int k = 0; k < 2; ++k) ok[k] = ok[k] && llf(qL[k], qR[k], n[k], gam, h[k]);
-        } else {
-            const bool r0 = roe(qL[0], qR[0], n[0], gam, h[0]);
-            const bool r1 = roe(qL[1], qR[1], n[1], gam, h[1]);
-            ok[0] = ok[0] && r0;
-            ok[1] = ok[1] && r1;
-        }
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            if (k == 1 && p0 + FACE_THREADS >= npairs) break;
-            if (!ok[k]) {
-                flag(err, 0, uint32_t(fid[k]));
-#pragma unroll
-                for (int v = 0; v < 5; ++v) h[k][v] = T(0);
+                for (int k = 0; k < 2; ++k) ok[k] = ok[k] && llf(qL[k], qR[k], n[k], gam, h[k]);
+            } else {
+                const bool r0 = roe(qL[0], qR[0], n[0], gam, h[0]);
+                const bool r1 = roe(qL[1], qR[1], n[1], gam, h[1]);
+                ok[0] = ok[0] && r0;
+                ok[1] = ok[1] && r1;
             }
 #pragma unroll
-            for (int v = 0; v < 5; ++v) hbuf[fid[k] * HS + v * NQF + qv[k]] = h[k][v];
+            for (int k = 0; k < 2; ++k) {
+                if (k == 1 && p0 + FACE_THREADS >= npairs) break;
+                if (!ok[k]) {
+                    flag(err, 0, uint32_t(fid[k]));
+#pragma unroll
+                    for (int v = 0; v < 5; ++v) h[k][v] = T(0);
+                }
+#pragma unroll
+                for (int v = 0; v < 5; ++v) hbuf[fid[k] * HS + v * NQF + qv[k]] = h[k][v];
+            }
         }
+        cur = nxt;
     }
 }
 
@@ -626,7 +660,16 @@ static int launch_face(const hodg_mesh_desc& m, const double* state, void* hbuf,
             return HODG_ECUDA;
         attr = true;
     }
-    const int64_t nblk = (fe - fb + FT - 1) / FT;
+    static int grid_cap = 0;
+    if (grid_cap == 0) {
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, face_flux_kernel<T>, FACE_THREADS, sm);
+        grid_cap = sms * (per_sm > 0 ? per_sm : 1);
+    }
+    const int64_t ntiles = (fe - fb + FT - 1) / FT;
+    const int64_t nblk = ntiles < grid_cap ? ntiles : grid_cap;  // persistent CTAs loop over tiles
     if (nblk > 0)
         face_flux_kernel<T><<<unsigned(nblk), FACE_THREADS, sm, st>>>(m, state, static_cast<T*>(hbuf), err, fb, fe);
     return cudaGetLastError() == cudaSuccess ? HODG_OK : HODG_ECUDA;
