@@ -12,7 +12,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_build", "libhodg_b200.so")
+LIB_PATH = os.environ.get("HODG_B200_LIB") or os.path.join(_HERE, "_build", "libhodg_b200.so")
 
 HODG_OK, HODG_EINVAL, HODG_ECUDA, HODG_ENODEV = 0, 2, 3, 4
 PREC_F64, PREC_MIXED = 64, 32

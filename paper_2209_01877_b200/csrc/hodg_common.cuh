@@ -119,13 +119,16 @@ __device__ __forceinline__ T prim(const T q[5], T g, T& u, T& v, T& w) {
 
 // Roe flux with Harten-Hyman entropy fix; hodg/physics.py:177-250 (3D).
 // Straight-line (no early returns, entropy fix as selects) so two calls
-// interleave; divisions are replaced by reciprocals of rho, (sL + sR) and
-// rsqrt(a2).  Returns ok = 0 on rho <= 0, p <= 0 or a2 <= 0 (then f is
+// interleave; divisions and square roots are replaced by rsqrt(rho) per
+// side (sqrt(rho) = rho rsqrt, 1/rho = rsqrt^2), 1/(sL + sR) and rsqrt(a2).  Returns ok = 0 on rho <= 0, p <= 0 or a2 <= 0 (then f is
 // garbage and the caller flags the face, as the reference's ok = 0).
 template <typename T>
 __device__ __forceinline__ bool roe(const T qL[5], const T qR[5], const T n[3], T g, T f[5]) {
     const T one = K<T>::one, half = K<T>::half;
-    const T riL = one / qL[0], riR = one / qR[0];
+    // one rsqrt per side gives both sqrt(rho) and 1/rho
+    const T isL = rsqrt(qL[0]), isR = rsqrt(qR[0]);
+    const T riL = isL * isL, riR = isR * isR;
+    const T sL = qL[0] * isL, sR = qR[0] * isR;
     const T uL = qL[1] * riL, vL = qL[2] * riL, wL = qL[3] * riL;
     const T uR = qR[1] * riR, vR = qR[2] * riR, wR = qR[3] * riR;
     const T gm1 = g - one;
@@ -134,8 +137,6 @@ __device__ __forceinline__ bool roe(const T qL[5], const T qR[5], const T n[3], 
     const T nx = n[0], ny = n[1], nz = n[2];
     const T vnL = uL * nx + vL * ny + wL * nz;
     const T vnR = uR * nx + vR * ny + wR * nz;
-    const T sL = sqrt(qL[0]);
-    const T sR = sqrt(qR[0]);
     const T di = one / (sL + sR);
     const T ut = (sL * uL + sR * uR) * di;
     const T vt = (sL * vL + sR * vR) * di;

@@ -193,29 +193,28 @@ __global__ void __launch_bounds__(FACE_THREADS, 4) face_flux_kernel(const hodg_m
         const Meta nxt = load_meta(tile + gridDim.x);  // in flight during this tile
         mbar_wait(bar + buf, (it >> 1) & 1);
 
-        // phase 1: traces of this side at all face qps for variables
-        // [VLO, VLO + NVG) (group g = 0: v 0..2, g = 1: v 3..4): each
-        // coefficient read from smem feeds NQF FMAs, each table value NVG
+        // phase 1: traces of this side at qps [g*QPT, g*QPT + QPT)
         const double* myrow = rows0 + buf * BUF + size_t(side * FT + lf) * RS;
-        constexpr int NV0 = 3;
-        const int vlo = g == 0 ? 0 : NV0;
-        T tr[NQF][NV0];
+        T tr[QPT][5];
 #pragma unroll
-        for (int q = 0; q < NQF; ++q)
+        for (int qq = 0; qq < QPT; ++qq)
 #pragma unroll
-            for (int k = 0; k < NV0; ++k) tr[q][k] = T(0);
+            for (int v = 0; v < 5; ++v) tr[qq][v] = T(0);
         if (cur.elem >= 0) {
             const T* fb = fbt + cur.slot * FBS;
 #pragma unroll
             for (int i = 0; i < NB; ++i) {
-                T c[NV0];
+                T c[5];
 #pragma unroll
-                for (int k = 0; k < NV0; ++k) c[k] = (g == 0 || k < 5 - NV0) ? T(myrow[(vlo + k) * NB + i]) : T(0);
+                for (int v = 0; v < 5; ++v) c[v] = T(myrow[v * NB + i]);
 #pragma unroll
-                for (int q = 0; q < NQF; ++q) {
-                    const T b = fb[q * NB + i];
+                for (int qq = 0; qq < QPT; ++qq) {
+                    const int q = g * QPT + qq;
+                    if (NG * QPT == NQF || q < NQF) {
+                        const T b = fb[q * NB + i];
 #pragma unroll
-                    for (int k = 0; k < NV0; ++k) tr[q][k] += b * c[k];
+                        for (int v = 0; v < 5; ++v) tr[qq][v] += b * c[v];
+                    }
                 }
             }
         }
@@ -223,10 +222,13 @@ __global__ void __launch_bounds__(FACE_THREADS, 4) face_flux_kernel(const hodg_m
         T* trs = reinterpret_cast<T*>(rows0 + buf * BUF);
         if (lf < nf) {
 #pragma unroll
-            for (int q = 0; q < NQF; ++q)
+            for (int qq = 0; qq < QPT; ++qq) {
+                const int q = g * QPT + qq;
+                if (NG * QPT == NQF || q < NQF) {
 #pragma unroll
-                for (int k = 0; k < NV0; ++k)
-                    if (g == 0 || k < 5 - NV0) trs[(size_t(side * FT + lf) * NQF + q) * 5 + vlo + k] = tr[q][k];
+                    for (int v = 0; v < 5; ++v) trs[(size_t(side * FT + lf) * NQF + q) * 5 + v] = tr[qq][v];
+                }
+            }
         }
         // next tile: its rows stream into the other buffer during phase 2
         if (tile + gridDim.x < ntiles) publish(nxt, buf ^ 1);
