@@ -55,6 +55,33 @@ __device__ __forceinline__ void sfor(F&& f) {
     sfor_impl(f, std::make_integer_sequence<int, N>{});
 }
 
+// load n consecutive doubles starting at a 16-byte aligned address with
+// 128-bit loads (conflict-free at the element kernel's row strides)
+template <int N>
+__device__ __forceinline__ void ld_row(const double* src, double (&dst)[N]) {
+#pragma unroll
+    for (int k = 0; k + 1 < N; k += 2) {
+        const double2 p = *reinterpret_cast<const double2*>(src + k);
+        dst[k] = p.x;
+        dst[k + 1] = p.y;
+    }
+    if constexpr (N % 2 == 1) dst[N - 1] = src[N - 1];
+}
+
+// a face record's NQF values at offset `off` (parity known at compile
+// time): 128-bit loads on the aligned pairs
+template <int NQ, int START>
+__device__ __forceinline__ void ld_rec(const double* rec, double (&dst)[NQ]) {
+    if constexpr (START == 1) dst[0] = rec[0];
+#pragma unroll
+    for (int q = START; q + 1 < NQ; q += 2) {
+        const double2 p = *reinterpret_cast<const double2*>(rec + q);
+        dst[q] = p.x;
+        dst[q + 1] = p.y;
+    }
+    if constexpr ((NQ - START) % 2 == 1) dst[NQ - 1] = rec[NQ - 1];
+}
+
 // exponent d of monomial i in the graded order (degree, then descending x,
 // then descending y): the reference's `_EXPONENTS` order (hodg/basis.py:21) in 3D
 __host__ __device__ constexpr int expt(int i, int d) {
@@ -311,7 +338,7 @@ __global__ void __launch_bounds__(FACE_THREADS, 4) face_flux_kernel(const hodg_m
 // Geometry tiles are field-major ([tile][field][E]) so every smem access in
 // the hot phases is unit-stride across the warp.
 template <typename T>
-__global__ void __launch_bounds__(ETHREADS) elem_stage_kernel(const hodg_mesh_desc m, const T* __restrict__ hbuf,
+__global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? 4 : 3) elem_stage_kernel(const hodg_mesh_desc m, const T* __restrict__ hbuf,
                                                               const hodg_stage_args a, uint32_t* __restrict__ err) {
     using L = ElemSmem<T>;
     constexpr int HS = hstride<T>();
@@ -362,12 +389,20 @@ __global__ void __launch_bounds__(ETHREADS) elem_stage_kernel(const hodg_mesh_de
     double c[NB];
     double u0r[(ORDER <= 2) ? NB : 1];
     if (live) {
+        if constexpr ((NB % 2) == 0) {
+            ld_row(S + e * RS + v * NB, c);  // rows 16-byte aligned when NB is even
+        } else {
 #pragma unroll
-        for (int i = 0; i < NB; ++i) c[i] = S[e * RS + v * NB + i];
+            for (int i = 0; i < NB; ++i) c[i] = S[e * RS + v * NB + i];
+        }
         if constexpr (ORDER <= 2) {
             if (need_u0) {
+                if constexpr ((NB % 2) == 0) {
+                    ld_row(a.u0 + gid * RS + v * NB, u0r);
+                } else {
 #pragma unroll
-                for (int i = 0; i < NB; ++i) u0r[i] = a.u0[gid * RS + v * NB + i];
+                    for (int i = 0; i < NB; ++i) u0r[i] = a.u0[gid * RS + v * NB + i];
+                }
             }
         }
     }
@@ -442,8 +477,14 @@ __global__ void __launch_bounds__(ETHREADS) elem_stage_kernel(const hodg_mesh_de
         sfor<4>([&](auto s) {
             const T* hrec = HT + size_t(s * E + e) * HSS + v * NQF;
             T hq[NQF];
+            if constexpr (sizeof(T) == 8) {
+                // record rows are 16-byte aligned: 128-bit loads on aligned pairs
+                if ((v * NQF) & 1) ld_rec<NQF, 1>(hrec, hq);
+                else ld_rec<NQF, 0>(hrec, hq);
+            } else {
 #pragma unroll
-            for (int q = 0; q < NQF; ++q) hq[q] = hrec[q];
+                for (int q = 0; q < NQF; ++q) hq[q] = hrec[q];
+            }
             T fa[NB];
 #pragma unroll
             for (int i = 0; i < NB; ++i) fa[i] = T(0);
