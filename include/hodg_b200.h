@@ -151,6 +151,31 @@ int64_t hodg_rcm_work_bytes(int64_t n, int64_t nnz);
 int hodg_rcm(int64_t n, const int64_t* indptr, const int64_t* indices, int64_t* forward, int64_t* inverse,
              void* work, void* stream);
 
+/* 2D table-driven path: the reference's own discretisation (triangles and
+ * bilinear quads, 4 variables, per-cell quadrature tables of
+ * hodg/geometry.py:120-220) with the argument lists of the reference kernels
+ * (device pointers; arrays at the kernel precision `prec` unless typed):
+ *   hodg2d_flux_pass  <- flux_pass (Euler)     hodg/dg.py:240-351
+ *   hodg2d_rhs_pass   <- rhs_pass (Euler)      hodg/dg.py:353-460
+ *   hodg2d_dt_pass    <- _dt_pass              hodg/timestepping.py:105-134
+ *   hodg2d_axpy       <- _axpy_state           hodg/timestepping.py:165-171
+ *   hodg2d_combine    <- _combine_state        hodg/timestepping.py:174-180
+ * Error flags are the reference's uint8 per-face / per-cell arrays. */
+int hodg2d_flux_pass(int prec, int64_t n_faces, int nqf, int nb, const void* coeffs, const void* fbL, const void* fbR,
+                     const int32_t* face_cells, const int8_t* bc_code, const void* fnx, const void* fny,
+                     const void* qinf, double gamma, int flux_kind, void* finv, uint8_t* errf, void* stream);
+int hodg2d_rhs_pass(int prec, int64_t n_cells, int nb, int nqv, int nqf, int maxf, const void* coeffs,
+                    const void* finv, const void* vol_w, const void* vol_basis, const void* vol_gx,
+                    const void* vol_gy, const int8_t* cell_nfaces, const int32_t* cell_faces,
+                    const int8_t* cell_fsign, const void* face_w, const void* fbL, const void* fbR,
+                    const double* minv64, double gamma, double* res, uint8_t* errc, void* stream);
+int hodg2d_dt_pass(int prec, int64_t n_cells, int nb, const void* coeffs, const double* basis_mean, const double* h,
+                   double gamma, double mu, double cfl, int order, double* out, uint8_t* errc, void* stream);
+int hodg2d_axpy(int prec, int64_t n_cells, int per_cell, const void* u, const double* r, const double* dtc, void* out,
+                void* stream);
+int hodg2d_combine(int prec, int64_t n_cells, int per_cell, const void* u, const void* u1, const double* r1,
+                   const double* dtc, void* out, void* stream);
+
 /* number of kernels this library launched since load (for gpu_launches) */
 int64_t hodg_launch_count(void);
 

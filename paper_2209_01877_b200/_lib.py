@@ -88,6 +88,11 @@ SIGNATURES = {
     "hodg_rcm_work_bytes": (I64, [I64, I64]),
     "hodg_rcm": (I32, [I64, P, P, P, P, P, P]),
     "hodg_launch_count": (I64, []),
+    "hodg2d_flux_pass": (I32, [I32, I64, I32, I32, P, P, P, P, P, P, P, P, D, I32, P, P, P]),
+    "hodg2d_rhs_pass": (I32, [I32, I64, I32, I32, I32, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, D, P, P, P]),
+    "hodg2d_dt_pass": (I32, [I32, I64, I32, P, P, P, D, D, D, I32, P, P, P]),
+    "hodg2d_axpy": (I32, [I32, I64, I32, P, P, P, P, P]),
+    "hodg2d_combine": (I32, [I32, I64, I32, P, P, P, P, P, P]),
 }
 
 _lib = None

@@ -33,6 +33,8 @@ struct hodg_mesh {
 
 static std::atomic<int64_t> g_launches{0};
 
+int64_t hodg_count_launch(int64_t n) { return g_launches += n; }
+
 static inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 
 namespace {
