@@ -118,7 +118,7 @@ def build_case(n, order, renumber, device):
         g = P.build_adjacency(mesh)
         perm = P.rcm(g)
         bw = (P.bandwidth(g), P.bandwidth(g, perm))
-        mesh = P.apply_permutation(mesh, perm)
+        mesh = P.apply_permutation(mesh, perm, device="cuda")  # face re-sort on the GPU
     gas = P.GasModel()
     geo = P.compute_geometry(mesh, order)
     bcs = P.BoundaryConditions(P.freestream_conserved(gas, 0.5, 0.0))

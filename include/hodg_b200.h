@@ -176,6 +176,21 @@ int hodg2d_axpy(int prec, int64_t n_cells, int per_cell, const void* u, const do
 int hodg2d_combine(int prec, int64_t n_cells, int per_cell, const void* u, const void* u1, const double* r1,
                    const double* dtc, void* out, void* stream);
 
+/* point evaluations of the device interface flux and boundary state
+ * (roe_flux / boundary_state, hodg/physics.py:436-479): qL, qR, q (n, 5),
+ * normals (n, 3), qf (5); ok[i] = 0 where the reference returns ok = 0 */
+int hodg_point_flux(int prec, int64_t n, const void* qL, const void* qR, const void* normals, double gamma,
+                    int flux_kind, void* out, uint8_t* ok, void* stream);
+int hodg_point_bstate(int prec, int64_t n, int kind, const void* q, const void* normals, const void* qf, double gamma,
+                      void* out, void* stream);
+
+/* device face re-sort of apply_permutation (hodg/renumber.py:224-231):
+ * order[k] = old id of the k-th face by (min, max) new incident element id
+ * then old id; new_lr (F, 2) int64 = new left / right (-1 -> left), work of
+ * hodg_face_sort_work_bytes(F) bytes */
+int64_t hodg_face_sort_work_bytes(int64_t n_faces);
+int hodg_face_sort(int64_t n_faces, int64_t n_cells, const int64_t* new_lr, int64_t* order, void* work, void* stream);
+
 /* number of kernels this library launched since load (for gpu_launches) */
 int64_t hodg_launch_count(void);
 

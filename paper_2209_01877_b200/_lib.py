@@ -88,6 +88,10 @@ SIGNATURES = {
     "hodg_rcm_work_bytes": (I64, [I64, I64]),
     "hodg_rcm": (I32, [I64, P, P, P, P, P, P]),
     "hodg_launch_count": (I64, []),
+    "hodg_point_flux": (I32, [I32, I64, P, P, P, D, I32, P, P, P]),
+    "hodg_point_bstate": (I32, [I32, I64, I32, P, P, P, D, P, P]),
+    "hodg_face_sort_work_bytes": (I64, [I64]),
+    "hodg_face_sort": (I32, [I64, I64, P, P, P, P]),
     "hodg2d_flux_pass": (I32, [I32, I64, I32, I32, P, P, P, P, P, P, P, P, D, I32, P, P, P]),
     "hodg2d_rhs_pass": (I32, [I32, I64, I32, I32, I32, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, D, P, P, P]),
     "hodg2d_dt_pass": (I32, [I32, I64, I32, P, P, P, D, D, D, I32, P, P, P]),

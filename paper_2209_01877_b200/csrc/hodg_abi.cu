@@ -102,6 +102,38 @@ __global__ void min_partial_kernel(const double* __restrict__ x, int64_t n, doub
 
 __global__ void fill_u64_kernel(unsigned long long* slot, unsigned long long bits) { *slot = bits; }
 
+// point evaluations of the device interface flux / boundary state (the
+// reference's roe_flux / boundary_state API, hodg/physics.py:436-479)
+template <typename T>
+__global__ void point_flux_kernel(int64_t n, const T* qL, const T* qR, const T* nrm, double gamma, int kind, T* out,
+                                  uint8_t* ok) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    T a[5], b[5], nn[3], f[5];
+    for (int v = 0; v < 5; ++v) {
+        a[v] = qL[5 * i + v];
+        b[v] = qR[5 * i + v];
+    }
+    for (int d = 0; d < 3; ++d) nn[d] = nrm[3 * i + d];
+    const bool good = kind == HODG_FLUX_LLF ? hodg::llf(a, b, nn, T(gamma), f) : hodg::roe(a, b, nn, T(gamma), f);
+    for (int v = 0; v < 5; ++v) out[5 * i + v] = f[v];
+    ok[i] = good ? 1 : 0;
+}
+
+template <typename T>
+__global__ void point_bstate_kernel(int64_t n, int kind, const T* q, const T* nrm, const T* qf, double gamma, T* out) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    T a[5], nn[3], f[5], o[5];
+    for (int v = 0; v < 5; ++v) {
+        a[v] = q[5 * i + v];
+        f[v] = qf[v];
+    }
+    for (int d = 0; d < 3; ++d) nn[d] = nrm[3 * i + d];
+    hodg::bstate(kind, a, nn, f, T(gamma), o);
+    for (int v = 0; v < 5; ++v) out[5 * i + v] = o[v];
+}
+
 }  // namespace
 
 extern "C" {
@@ -286,5 +318,33 @@ int hodg_rcm(int64_t n, const int64_t* indptr, const int64_t* indices, int64_t* 
 }
 
 int64_t hodg_launch_count(void) { return g_launches.load(); }
+
+int hodg_point_flux(int prec, int64_t n, const void* qL, const void* qR, const void* normals, double gamma,
+                    int flux_kind, void* out, uint8_t* ok, void* stream) {
+    if (n <= 0 || !qL || !qR || !normals || !out || !ok) return HODG_EINVAL;
+    g_launches++;
+    const unsigned nb = unsigned((n + 127) / 128);
+    if (prec == HODG_PREC_F64)
+        point_flux_kernel<double><<<nb, 128, 0, S(stream)>>>(n, (const double*)qL, (const double*)qR,
+                                                             (const double*)normals, gamma, flux_kind, (double*)out, ok);
+    else
+        point_flux_kernel<float><<<nb, 128, 0, S(stream)>>>(n, (const float*)qL, (const float*)qR,
+                                                            (const float*)normals, gamma, flux_kind, (float*)out, ok);
+    return cudaGetLastError() == cudaSuccess ? HODG_OK : HODG_ECUDA;
+}
+
+int hodg_point_bstate(int prec, int64_t n, int kind, const void* q, const void* normals, const void* qf, double gamma,
+                      void* out, void* stream) {
+    if (n <= 0 || !q || !normals || !qf || !out) return HODG_EINVAL;
+    g_launches++;
+    const unsigned nb = unsigned((n + 127) / 128);
+    if (prec == HODG_PREC_F64)
+        point_bstate_kernel<double><<<nb, 128, 0, S(stream)>>>(n, kind, (const double*)q, (const double*)normals,
+                                                               (const double*)qf, gamma, (double*)out);
+    else
+        point_bstate_kernel<float><<<nb, 128, 0, S(stream)>>>(n, kind, (const float*)q, (const float*)normals,
+                                                              (const float*)qf, gamma, (float*)out);
+    return cudaGetLastError() == cudaSuccess ? HODG_OK : HODG_ECUDA;
+}
 
 }  // extern "C"

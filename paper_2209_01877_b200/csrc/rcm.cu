@@ -362,3 +362,54 @@ int hodg_rcm_impl(int64_t n, const int64_t* indptr, const int64_t* indices, int6
     if (launches) *launches = cx.launches;
     return cudaGetLastError() == cudaSuccess ? HODG_OK : HODG_ECUDA;
 }
+
+// ---------------------------------------------------------------------------
+// Face re-sort of apply_permutation (hodg/renumber.py:224-231): stable sort
+// of the faces by the packed key (min, max) of the new incident element ids
+// (boundary faces use right = left).  A stable LSD radix sort of the key with
+// the old face id as the value reproduces numpy's lexsort((ids, kmax, kmin)).
+namespace {
+__global__ void face_keys_kernel(int64_t nf, int64_t n, const int64_t* __restrict__ lr,
+                                 unsigned long long* __restrict__ keys, int64_t* __restrict__ ids) {
+    const int64_t f = int64_t(blockIdx.x) * TPB + threadIdx.x;
+    if (f >= nf) return;
+    const int64_t l = lr[2 * f];
+    const int64_t r = lr[2 * f + 1] >= 0 ? lr[2 * f + 1] : l;
+    const int64_t lo = l < r ? l : r, hi = l < r ? r : l;
+    keys[f] = (unsigned long long)lo * (unsigned long long)(n + 1) + (unsigned long long)hi;
+    ids[f] = f;
+}
+}  // namespace
+
+int64_t hodg_face_sort_work_bytes(int64_t nf) {
+    size_t b = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, b, (unsigned long long*)nullptr, (unsigned long long*)nullptr,
+                                    (int64_t*)nullptr, (int64_t*)nullptr, int(nf > 0 ? nf : 1), 0, 64);
+    return int64_t(3 * al(size_t(nf) * 8) + al(b) + 256);
+}
+
+extern int64_t hodg_count_launch(int64_t n);
+
+extern "C" int hodg_face_sort(int64_t nf, int64_t n, const int64_t* lr, int64_t* order, void* work,
+                              void* stream) {
+    if (nf <= 0 || n <= 0 || !lr || !order || !work) return HODG_EINVAL;
+    if (nf >= (1ll << 31)) return HODG_EINVAL;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    char* p = static_cast<char*>(work);
+    auto* k0 = reinterpret_cast<unsigned long long*>(p);
+    p += al(size_t(nf) * 8);
+    auto* k1 = reinterpret_cast<unsigned long long*>(p);
+    p += al(size_t(nf) * 8);
+    auto* ids = reinterpret_cast<int64_t*>(p);
+    p += al(size_t(nf) * 8);
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, k0, k1, ids, order, int(nf), 0, 64, st);
+    face_keys_kernel<<<nb(nf), TPB, 0, st>>>(nf, n, lr, k0, ids);
+    int end_bit = 1;  // significant key bits: key < (n + 1)^2
+    while (end_bit < 64 && ((unsigned long long)1 << end_bit) <= (unsigned long long)(n + 1) * (unsigned long long)(n + 1))
+        ++end_bit;
+    if (cub::DeviceRadixSort::SortPairs(p, tb, k0, k1, ids, order, int(nf), 0, end_bit, st) != cudaSuccess)
+        return HODG_ECUDA;
+    hodg_count_launch(2);
+    return cudaGetLastError() == cudaSuccess ? HODG_OK : HODG_ECUDA;
+}

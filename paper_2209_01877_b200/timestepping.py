@@ -414,7 +414,7 @@ def run(config: RunConfig, mesh: TetMesh | None = None) -> RunArtifacts:
         g = build_adjacency(mesh)
         perm = rcm(g)
         bw0, bw1 = bandwidth(g), bandwidth(g, perm)
-        mesh = apply_permutation(mesh, perm)
+        mesh = apply_permutation(mesh, perm, device="cuda")
     geo = compute_geometry(mesh, config.order)
     state = project_initial(mesh, geo, initial_field(config, gas), gas)
     disc = _get_disc(mesh, geo, gas, bcs)

@@ -1,0 +1,132 @@
+"""Device point physics vs the oracle, and the reference's flux property
+suite restated in 3D (pkg/tests/test_physics.py:167-210, acceptance c05 on
+10^4 states); device face re-sort; discretisation order (test_dg.py:257-272)."""
+
+import numpy as np
+import pytest
+
+from oracle import solver as S
+
+pytestmark = pytest.mark.gpu
+
+
+def random_states(n, seed):
+    rng = np.random.default_rng(seed)
+    rho = rng.uniform(0.2, 3.0, n)
+    vel = rng.uniform(-2.0, 2.0, (n, 3))
+    p = rng.uniform(0.2, 3.0, n)
+    e = p / 0.4 + 0.5 * rho * np.einsum("nd,nd->n", vel, vel)
+    return np.column_stack([rho, rho * vel, e])
+
+
+def unit(n, seed):
+    v = np.random.default_rng(seed).normal(size=(n, 3))
+    return v / np.linalg.norm(v, axis=1)[:, None]
+
+
+def phys_flux(q, nrm, g=1.4):
+    rho, m, E = q[:, 0], q[:, 1:4], q[:, 4]
+    vel = m / rho[:, None]
+    p = (g - 1.0) * (E - 0.5 * rho * np.einsum("nd,nd->n", vel, vel))
+    vn = np.einsum("nd,nd->n", vel, nrm)
+    return np.column_stack([rho * vn, m * vn[:, None] + p[:, None] * nrm, (E + p) * vn])
+
+
+@pytest.fixture(scope="module")
+def PW():
+    from paper_2209_01877_b200 import pointwise
+
+    return pointwise
+
+
+@pytest.mark.parametrize("flux,kind", [("roe", 0), ("llf", 1)])
+def test_point_flux_matches_oracle(PW, flux, kind):
+    n = 10000
+    qL, qR, nr = random_states(n, 1), random_states(n, 2), unit(n, 3)
+    f, ok = PW.point_flux(qL, qR, nr, flux=flux)
+    ref, rok = S.point_flux(qL, qR, nr, flux_kind=kind)
+    assert np.array_equal(ok, rok)
+    scale = np.abs(ref).max(axis=1, keepdims=True)
+    assert np.abs(f - ref).max() / scale.max() < 1e-14
+    assert (np.abs(f - ref) / scale).max() < 1e-13
+
+
+@pytest.mark.parametrize("kind", ["far_field", "slip_wall", "no_slip_wall"])
+def test_boundary_states_match_oracle(PW, kind):
+    n = 10000
+    q, nr = random_states(n, 4), unit(n, 5)
+    fs = S.freestream_conserved(S.Gas(), 0.5, 10.0, 3)
+    b = PW.point_bstate(kind, q, nr, fs)
+    ref = S.point_bstate({"far_field": 1, "slip_wall": 2, "no_slip_wall": 3}[kind], q, nr, fs)
+    assert np.abs(b - ref).max() / np.abs(ref).max() < 1e-14
+
+
+def test_flux_properties(PW):
+    """consistency, conservation, supersonic upwinding, slip-wall mass flux."""
+    n = 10000
+    q, q2, nr = random_states(n, 6), random_states(n, 7), unit(n, 8)
+    f, ok = PW.point_flux(q, q, nr)
+    assert ok.all()
+    ff = phys_flux(q, nr)
+    assert np.abs(f - ff).max() / np.abs(ff).max() < 1e-13
+    a, _ = PW.point_flux(q, q2, nr)
+    b, _ = PW.point_flux(q2, q, -nr)
+    assert np.abs(a + b).max() / np.abs(a).max() < 1e-13
+    # supersonic along n: the Roe flux is the upwind physical flux
+    rho = np.full(n, 1.0)
+    vel = nr * 3.0
+    p = np.full(n, 0.5)
+    qs = np.column_stack([rho, rho[:, None] * vel, p / 0.4 + 0.5 * rho * 9.0])
+    qs2 = qs.copy()
+    qs2[:, 0] *= 1.01
+    qs2[:, 4] *= 1.01
+    fu, _ = PW.point_flux(qs, qs2, nr)
+    assert np.abs(fu - phys_flux(qs, nr)).max() / np.abs(fu).max() < 1e-13
+    # slip wall: zero mass flux through the wall
+    w = PW.point_bstate("slip_wall", q, nr, q[0])
+    fw, _ = PW.point_flux(q, w, nr)
+    assert np.abs(fw[:, 0]).max() < 1e-12
+
+
+def test_inadmissible_states_flagged(PW):
+    q = random_states(4, 9)
+    bad = q.copy()
+    bad[0, 0] = -1.0
+    bad[1, 4] = 0.0  # negative pressure
+    _, ok = PW.point_flux(q, bad, unit(4, 1))
+    assert not ok[0] and not ok[1] and ok[2] and ok[3]
+
+
+def test_device_face_sort_matches_numpy():
+    import paper_2209_01877_b200 as P
+
+    m = P.generate_tet_box(6)
+    perm = P.random_permutation(m.n_cells, 3)
+    a = P.apply_permutation(m, perm)
+    b = P.apply_permutation(m, perm, device="cuda")
+    for k in ("face_cells", "face_nodes", "cell_faces", "face_normal"):
+        assert np.array_equal(getattr(a, k), getattr(b, k)), k
+
+
+@pytest.mark.parametrize("order,min_rate", [(1, 1.5), (2, 2.5)])
+def test_projected_steady_vortex_residual_order(order, min_rate):
+    """A vortex tube with zero advection is a steady exact solution; the
+    residual of its projection is truncation error and must shrink at the
+    discretisation order (the 3D analogue of pkg/tests/test_dg.py:257-272)."""
+    import paper_2209_01877_b200 as P
+
+    gas = P.GasModel()
+    errs = []
+    for n in (6, 12):
+        m = P.generate_tet_box(n, n, 2, extent=(0.0, 0.0, 0.0, 10.0, 10.0, 10.0 / n * 2),
+                               bc={"xmin": "far_field", "xmax": "far_field", "ymin": "far_field",
+                                   "ymax": "far_field", "zmin": "slip_wall", "zmax": "slip_wall"})
+        geo = P.compute_geometry(m, order)
+        bcs = P.BoundaryConditions(P.freestream_conserved(gas, 1e-12, 0.0))
+        st = P.project_initial(m, geo, lambda x, y, z: P.vortex_primitive(gas, 1e-12, 0.0, 5.0, 5.0, 5.0, 0.0, x, y),
+                               gas)
+        r = P.rhs(st, m, geo, bcs, gas)
+        errs.append(np.linalg.norm(P.residual_l2(r, m)))
+    rate = np.log2(errs[0] / errs[1])
+    print(f"P{order} residual convergence rate {rate:.2f}")
+    assert rate > min_rate
