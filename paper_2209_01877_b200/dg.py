@@ -43,6 +43,7 @@ __all__ = [
     "accumulate_rhs",
     "rhs",
     "cell_means",
+    "density_l2_error",
 ]
 
 N_VARS = 5
@@ -330,3 +331,21 @@ def cell_means(state: DofState, geo: DeviceGeometry):
     t = ref_tables(geo.order)
     mean = _torch().from_numpy(t.MEAN).to(disc.device)
     return rows[:, : N_VARS * t.nb].reshape(disc.n, N_VARS, t.nb) @ mean
+
+
+def density_l2_error(state: DofState, mesh: TetMesh, geo: DeviceGeometry, rho_exact) -> float:
+    """Quadrature L2 norm of the density error against rho_exact(x, y, z)
+    (hodg/dg.py:671-677), evaluating the Taylor expansion at the volume
+    quadrature points."""
+    from .basis import exponents
+    from .refelem import monomials
+
+    t = ref_tables(geo.order)
+    pts = volume_points(mesh, geo.order)
+    X = (pts - mesh.cell_centroid[:, None, :]) / mesh.cell_h[:, None, None]
+    B = monomials(exponents(3, geo.order), X)
+    c = state.coeffs[:, 0, :].double().cpu().numpy()
+    rho_h = np.einsum("nqj,nj->nq", B, c)
+    err = rho_h - rho_exact(pts[..., 0], pts[..., 1], pts[..., 2])
+    w = t.vol_weights[None, :] * mesh.cell_area[:, None]
+    return float(np.sqrt(np.sum(w * err * err)))
