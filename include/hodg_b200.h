@@ -126,9 +126,11 @@ int64_t hodg_stage_blocks(const hodg_mesh* mesh, int prec); /* rows of norm_part
 int hodg_face_flux(const hodg_mesh* mesh, int prec, const double* state, void* face_buf, uint32_t* err,
                    void* stream);
 /* faces [f_begin, f_end) only: lets a partitioned run evaluate interior
- * faces while the halo exchange is in flight, then the partition faces */
+ * faces while the halo exchange is in flight, then the partition faces.
+ * interior_only = 1 promises every face in the range has a right element
+ * and selects the kernel variant without the boundary-state code. */
 int hodg_face_flux_range(const hodg_mesh* mesh, int prec, const double* state, void* face_buf, int64_t f_begin,
-                         int64_t f_end, uint32_t* err, void* stream);
+                         int64_t f_end, int interior_only, uint32_t* err, void* stream);
 int hodg_elem_stage(const hodg_mesh* mesh, int prec, const void* face_buf, const hodg_stage_args* args,
                     uint32_t* err, void* stream);
 int hodg_local_dt(const hodg_mesh* mesh, const double* state, double cfl, double* dt_vec_out,

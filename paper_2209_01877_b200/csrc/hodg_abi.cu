@@ -11,7 +11,7 @@
 
 #define DECL_ORDER(P)                                                                                          \
     int hodg_launch_face_p##P(const hodg_mesh_desc&, int, const double*, void*, uint32_t*, cudaStream_t, int64_t, \
-                              int64_t);                                                                        \
+                              int64_t, int);                                                                   \
     int hodg_launch_elem_p##P(const hodg_mesh_desc&, int, const void*, const hodg_stage_args&, uint32_t*,      \
                               cudaStream_t);                                                                   \
     int hodg_launch_dt_p##P(const hodg_mesh_desc&, const double*, double, double*, unsigned long long*,        \
@@ -191,7 +191,7 @@ int64_t hodg_stage_blocks(const hodg_mesh* mesh, int prec) {
 }
 
 int hodg_face_flux_range(const hodg_mesh* mesh, int prec, const double* state, void* face_buf, int64_t f_begin,
-                         int64_t f_end, uint32_t* err, void* stream) {
+                         int64_t f_end, int interior_only, uint32_t* err, void* stream) {
     if (!mesh || !state || !face_buf) return HODG_EINVAL;
     if (prec != HODG_PREC_F64 && prec != HODG_PREC_MIXED) return HODG_EINVAL;
     if (f_begin < 0 || f_end > mesh->d.n_faces || f_begin > f_end) return HODG_EINVAL;
@@ -199,17 +199,17 @@ int hodg_face_flux_range(const hodg_mesh* mesh, int prec, const double* state, v
     g_launches++;
     const hodg_mesh_desc& d = mesh->d;
     switch (d.order) {
-        case 0: return hodg_launch_face_p0(d, prec, state, face_buf, err, S(stream), f_begin, f_end);
-        case 1: return hodg_launch_face_p1(d, prec, state, face_buf, err, S(stream), f_begin, f_end);
-        case 2: return hodg_launch_face_p2(d, prec, state, face_buf, err, S(stream), f_begin, f_end);
-        default: return hodg_launch_face_p3(d, prec, state, face_buf, err, S(stream), f_begin, f_end);
+        case 0: return hodg_launch_face_p0(d, prec, state, face_buf, err, S(stream), f_begin, f_end, interior_only);
+        case 1: return hodg_launch_face_p1(d, prec, state, face_buf, err, S(stream), f_begin, f_end, interior_only);
+        case 2: return hodg_launch_face_p2(d, prec, state, face_buf, err, S(stream), f_begin, f_end, interior_only);
+        default: return hodg_launch_face_p3(d, prec, state, face_buf, err, S(stream), f_begin, f_end, interior_only);
     }
 }
 
 int hodg_face_flux(const hodg_mesh* mesh, int prec, const double* state, void* face_buf, uint32_t* err,
                    void* stream) {
     if (!mesh) return HODG_EINVAL;
-    return hodg_face_flux_range(mesh, prec, state, face_buf, 0, mesh->d.n_faces, err, stream);
+    return hodg_face_flux_range(mesh, prec, state, face_buf, 0, mesh->d.n_faces, 0, err, stream);
 }
 
 int hodg_elem_stage(const hodg_mesh* mesh, int prec, const void* face_buf, const hodg_stage_args* a, uint32_t* err,

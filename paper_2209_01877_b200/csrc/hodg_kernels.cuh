@@ -133,7 +133,7 @@ __host__ __device__ constexpr size_t elem_smem_bytes() {
 //           across the 5 variables);
 //  phase 2: thread (face, qp) closes boundary faces with the BC state and
 //           evaluates the Roe / LLF flux, writing H[f][v][q] (padded record).
-template <typename T>
+template <typename T, bool BND>
 __global__ void __launch_bounds__(FACE_THREADS, 4) face_flux_kernel(const hodg_mesh_desc m,
                                                                     const double* __restrict__ state,
                                                                     T* __restrict__ hbuf,
@@ -282,10 +282,10 @@ __global__ void __launch_bounds__(FACE_THREADS, 4) face_flux_kernel(const hodg_m
 #pragma unroll
                 for (int v = 0; v < 5; ++v) qL[k][v] = trs[(size_t(lfp) * NQF + q) * 5 + v];
                 ok[k] = true;
-                if (info & 0x100) {
+                if (!BND || (info & 0x100)) {
 #pragma unroll
                     for (int v = 0; v < 5; ++v) qR[k][v] = trs[(size_t(FT + lfp) * NQF + q) * 5 + v];
-                } else {
+                } else if constexpr (BND) {
                     T u, vv, w;
                     if (!(qL[k][0] > T(0)) || !(prim(qL[k], gam, u, vv, w) > T(0))) {
                         ok[k] = false;
@@ -690,13 +690,13 @@ __global__ void modal_transform_kernel(const hodg_mesh_desc m, int to_reference,
 namespace hodg {
 namespace HODG_CAT(ord, ORDER) {
 
-template <typename T>
-static int launch_face(const hodg_mesh_desc& m, const double* state, void* hbuf, uint32_t* err, cudaStream_t st,
-                       int64_t fb, int64_t fe) {
+template <typename T, bool BND>
+static int launch_face_k(const hodg_mesh_desc& m, const double* state, void* hbuf, uint32_t* err, cudaStream_t st,
+                         int64_t fb, int64_t fe) {
     const size_t sm = face_smem_bytes<T>();
     static bool attr = false;
     if (!attr) {
-        if (cudaFuncSetAttribute(face_flux_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)) !=
+        if (cudaFuncSetAttribute(face_flux_kernel<T, BND>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)) !=
             cudaSuccess)
             return HODG_ECUDA;
         attr = true;
@@ -706,14 +706,24 @@ static int launch_face(const hodg_mesh_desc& m, const double* state, void* hbuf,
         int dev = 0, sms = 0, per_sm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, face_flux_kernel<T>, FACE_THREADS, sm);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, face_flux_kernel<T, BND>, FACE_THREADS, sm);
         grid_cap = sms * (per_sm > 0 ? per_sm : 1);
     }
     const int64_t ntiles = (fe - fb + FT - 1) / FT;
     const int64_t nblk = ntiles < grid_cap ? ntiles : grid_cap;  // persistent CTAs loop over tiles
     if (nblk > 0)
-        face_flux_kernel<T><<<unsigned(nblk), FACE_THREADS, sm, st>>>(m, state, static_cast<T*>(hbuf), err, fb, fe);
+        face_flux_kernel<T, BND>
+            <<<unsigned(nblk), FACE_THREADS, sm, st>>>(m, state, static_cast<T*>(hbuf), err, fb, fe);
     return cudaGetLastError() == cudaSuccess ? HODG_OK : HODG_ECUDA;
+}
+
+// interior_only: every face in [fb, fe) has a right element (no boundary
+// state code in the kernel)
+template <typename T>
+static int launch_face(const hodg_mesh_desc& m, const double* state, void* hbuf, uint32_t* err, cudaStream_t st,
+                       int64_t fb, int64_t fe, int interior_only) {
+    return interior_only ? launch_face_k<T, false>(m, state, hbuf, err, st, fb, fe)
+                         : launch_face_k<T, true>(m, state, hbuf, err, st, fb, fe);
 }
 
 template <typename T>
@@ -738,10 +748,10 @@ static int launch_elem(const hodg_mesh_desc& m, const void* hbuf, const hodg_sta
 
 extern "C++" {
 int HODG_CAT(hodg_launch_face_p, ORDER)(const hodg_mesh_desc& m, int prec, const double* state, void* hbuf,
-                                         uint32_t* err, cudaStream_t st, int64_t fb, int64_t fe) {
+                                         uint32_t* err, cudaStream_t st, int64_t fb, int64_t fe, int interior) {
     using namespace hodg::HODG_CAT(ord, ORDER);
-    return prec == HODG_PREC_MIXED ? launch_face<float>(m, state, hbuf, err, st, fb, fe)
-                                   : launch_face<double>(m, state, hbuf, err, st, fb, fe);
+    return prec == HODG_PREC_MIXED ? launch_face<float>(m, state, hbuf, err, st, fb, fe, interior)
+                                   : launch_face<double>(m, state, hbuf, err, st, fb, fe, interior);
 }
 
 int HODG_CAT(hodg_launch_elem_p, ORDER)(const hodg_mesh_desc& m, int prec, const void* hbuf,

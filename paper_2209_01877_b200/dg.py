@@ -214,11 +214,19 @@ class Discretization:
             raise AdmissibilityError("inadmissible cell mean", cell=int(idv.value), iteration=iteration)
 
     def face_flux(self, rows, prec, hbuf=None, stream=None, f_begin=0, f_end=None):
+        """Face kernel over device faces [f_begin, f_end): interior ranges use
+        the kernel variant without boundary states, the boundary range the
+        general one."""
         hbuf = self.face_buffer(prec) if hbuf is None else hbuf
         f_end = self.nf if f_end is None else f_end
-        _lib.check(self.L.hodg_face_flux_range(self.handle, prec, _lib.ptr(rows), _lib.ptr(hbuf), int(f_begin),
-                                               int(f_end), _lib.ptr(self.err), _lib.stream_ptr(stream)),
-                   "hodg_face_flux_range")
+        g = self.geo
+        b0, b1 = g.n_int0, g.n_int0 + g.n_bnd
+        for lo, hi, interior in ((0, b0, 1), (b0, b1, 0), (b1, self.nf, 1)):
+            lo, hi = max(lo, f_begin), min(hi, f_end)
+            if hi > lo:
+                _lib.check(self.L.hodg_face_flux_range(self.handle, prec, _lib.ptr(rows), _lib.ptr(hbuf), int(lo),
+                                                       int(hi), interior, _lib.ptr(self.err),
+                                                       _lib.stream_ptr(stream)), "hodg_face_flux_range")
         return hbuf
 
     def stage(self, prec, hbuf, args: _lib.StageArgs, stream=None):
@@ -288,7 +296,8 @@ def face_flux_pass(state: DofState, aux, mesh: TetMesh, geo: DeviceGeometry, bcs
     hbuf = disc.face_flux(rows, prec, hbuf=_torch().empty_like(disc.face_buffer(prec)))
     disc.raise_errors(state.iteration)
     h = hbuf[:, : N_VARS * disc.nqf].reshape(disc.nf, N_VARS, disc.nqf)
-    return FaceFluxBuffer(inviscid=h.transpose(1, 2))
+    inv = _torch().as_tensor(geo.face_inv, device=disc.device)
+    return FaceFluxBuffer(inviscid=h.index_select(0, inv).transpose(1, 2))  # mesh face order
 
 
 def accumulate_rhs(state: DofState, aux, fluxes: FaceFluxBuffer, mesh: TetMesh, geo: DeviceGeometry,
@@ -300,8 +309,9 @@ def accumulate_rhs(state: DofState, aux, fluxes: FaceFluxBuffer, mesh: TetMesh, 
     rows = disc.to_reference(state.coeffs)
     dt = torch.float32 if prec == _lib.PREC_MIXED else torch.float64
     hbuf = torch.zeros_like(disc.face_buffer(prec))
-    hbuf[:, : N_VARS * disc.nqf] = torch.as_tensor(fluxes.inviscid, device=disc.device).to(dt).transpose(
-        1, 2).reshape(disc.nf, -1)
+    perm = torch.as_tensor(geo.face_perm, device=disc.device)
+    h = torch.as_tensor(fluxes.inviscid, device=disc.device).to(dt).index_select(0, perm)  # device face order
+    hbuf[:, : N_VARS * disc.nqf] = h.transpose(1, 2).reshape(disc.nf, -1)
     disc.reset_errors()
     res = disc.residual_rows(rows, hbuf, prec)
     disc.raise_errors(state.iteration)

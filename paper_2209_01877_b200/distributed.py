@@ -101,7 +101,7 @@ def setup_partitioned(mesh: TetMesh, order: int, gas: GasModel, bcs: BoundaryCon
     """RCB partition of `mesh` over `world` ranks -> (LocalPart, Discretization)."""
     parts = rcb_partition(mesh.cell_centroid, world)
     part = build_local(mesh, parts, rank)
-    geo = compute_geometry(part.mesh, order)
+    geo = compute_geometry(part.mesh, order, split=part.n_inner_faces)
     disc = Discretization(part.mesh, geo, gas, bcs, device=device, n_elems=part.n_owned)
     return part, disc
 

@@ -55,6 +55,10 @@ class DeviceGeometry:
     fcells: np.ndarray
     finfo: np.ndarray
     fnrm: np.ndarray
+    face_perm: np.ndarray = None  # device face k is mesh face face_perm[k]
+    face_inv: np.ndarray = None  # mesh face j is device face face_inv[j]
+    n_int0: int = 0  # device faces [0, n_int0): interior
+    n_bnd: int = 0  # [n_int0, n_int0 + n_bnd): boundary; the rest: interior (partition faces)
     _dev: dict = field(default_factory=dict, repr=False)
     _disc_cache: dict = field(default_factory=dict, repr=False)
 
@@ -87,7 +91,12 @@ def element_jacobians(mesh: TetMesh):
     return V, J
 
 
-def compute_geometry(mesh: TetMesh, order: int) -> DeviceGeometry:
+def compute_geometry(mesh: TetMesh, order: int, split: int | None = None) -> DeviceGeometry:
+    """Device geometry.  Faces are laid out [interior | boundary | interior
+    tail]: mesh faces [0, split) split into interior then boundary faces
+    (order kept within each class), mesh faces [split, F) -- a partition's
+    ghost faces, all interior -- after them; the interior ranges run the
+    face-kernel variant without boundary-state code."""
     if order not in (0, 1, 2, 3):
         raise GeometryError(f"unsupported order {order}; expected 0..3")
     codes = mesh.boundary_kind_codes()
@@ -110,14 +119,26 @@ def compute_geometry(mesh: TetMesh, order: int) -> DeviceGeometry:
     econv = np.empty((n, 18))
     econv[:, 0:9] = (J / h[:, None, None]).reshape(n, 9)
     econv[:, 9:18] = (Jinv * h[:, None, None]).reshape(n, 9)
-    slots = mesh.face_slots.astype(np.int32)
-    finfo = (slots[:, 0] | (np.maximum(slots[:, 1], 0) << 2) | (codes.astype(np.int32) << 4)).astype(np.int32)
-    fnrm = np.zeros((mesh.n_faces, 4))
-    fnrm[:, :3] = mesh.face_normal
+    F = mesh.n_faces
+    split = F if split is None else int(split)
+    ids = np.arange(F)
+    bnd = mesh.face_cells[:, 1] < 0
+    if np.any(bnd[split:]):
+        raise GeometryError("faces past the split must be interior")
+    head = ids[:split]
+    perm = np.concatenate([head[~bnd[:split]], head[bnd[:split]], ids[split:]])
+    inv = np.empty(F, dtype=np.int64)
+    inv[perm] = np.arange(F)
+    slots = mesh.face_slots.astype(np.int32)[perm]
+    finfo = (slots[:, 0] | (np.maximum(slots[:, 1], 0) << 2) | (codes[perm].astype(np.int32) << 4)).astype(np.int32)
+    fnrm = np.zeros((F, 4))
+    fnrm[:, :3] = mesh.face_normal[perm]
     T = TILE[order]
-    return DeviceGeometry(order, ref_tables(order).nb, tile_major(egeo, T), econv,
-                          tile_major(mesh.cell_faces.astype(np.int32), T), mesh.face_cells.astype(np.int32), finfo,
-                          fnrm)
+    efaces = inv[mesh.cell_faces.astype(np.int64)].astype(np.int32)
+    efaces[mesh.cell_faces < 0] = 0
+    return DeviceGeometry(order, ref_tables(order).nb, tile_major(egeo, T), econv, tile_major(efaces, T),
+                          mesh.face_cells.astype(np.int32)[perm], finfo, fnrm, perm, inv,
+                          int(np.count_nonzero(~bnd[:split])), int(np.count_nonzero(bnd[:split])))
 
 
 def volume_points(mesh: TetMesh, order: int) -> np.ndarray:

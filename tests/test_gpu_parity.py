@@ -231,7 +231,8 @@ def test_partitioned_residual_bitwise_on_one_gpu(P, nparts):
     parts = rcb_partition(m.cell_centroid, nparts)
     for r in range(nparts):
         part = build_local(m, parts, r)
-        d = Discretization(part.mesh, compute_geometry(part.mesh, order), gas, bcs, n_elems=part.n_owned)
+        d = Discretization(part.mesh, compute_geometry(part.mesh, order, split=part.n_inner_faces), gas, bcs,
+                           n_elems=part.n_owned)
         gl = torch.as_tensor(np.concatenate([part.owned, part.ghosts]), device="cuda")
         rows = rows_g.index_select(0, gl).contiguous()  # owned + ghost rows (the halo)
         hb = d.face_buffer(64)
