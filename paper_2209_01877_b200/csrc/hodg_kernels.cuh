@@ -24,10 +24,18 @@ constexpr int QPT = (NQF + NG - 1) / NG;     // face qps per phase-1 thread
 constexpr int FACE_THREADS = 128;
 constexpr int FT = FACE_THREADS / (2 * NG);  // faces per CTA (32 for P1-P3)
 constexpr int FBS = NQF * NB + 1;            // padded per-slot stride of the smem trace table
+#ifdef HODG_E2_OVERRIDE
+constexpr int E = (ORDER >= 3) ? 16 : (ORDER == 2 ? HODG_E2_OVERRIDE : 64);
+#else
 constexpr int E = (ORDER >= 3) ? 16 : (ORDER == 2 ? 32 : 64);  // elements per CTA
+#endif
 constexpr int ETHREADS = 5 * E;
 constexpr int XS = 15;                        // smem slot per (element, qp): 5 traces -> 15 contravariant fluxes
+#ifdef HODG_QC2_OVERRIDE
+constexpr int QC = (NQV <= 8) ? NQV : (ORDER == 2 ? HODG_QC2_OVERRIDE : 8);
+#else
 constexpr int QC = (NQV <= 8) ? NQV : (ORDER == 2 ? 7 : 8);  // volume qps per chunk (bounds the X buffer)
+#endif
 constexpr int NCH = (NQV + QC - 1) / QC;
 
 // padded per-face record of the face flux buffer: 5 x NQF values rounded up
