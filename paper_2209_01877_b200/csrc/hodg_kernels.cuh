@@ -419,6 +419,9 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? 4 : 3) elem_stage_k
     T acc[NB];
 #pragma unroll
     for (int i = 0; i < NB; ++i) acc[i] = T(0);
+    T ji[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) ji[k] = T(G[k * E + e]);
     const T gam = T(m.gamma);
     sfor<NCH>([&](auto ch) {
         constexpr int q0 = ch * QC;
@@ -449,23 +452,33 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? 4 : 3) elem_stage_k
                 for (int k = 0; k < XS; ++k) sl[k] = T(0);
                 continue;
             }
+            // physical flux F[d][var]; the reference-frame map J^-1 F is
+            // applied per variable in phase C (balanced across threads)
             const T Hs = U[4] + pr;
-            const T F[3][5] = {{U[1], U[1] * u + pr, U[1] * vv, U[1] * w, Hs * u},
-                               {U[2], U[2] * u, U[2] * vv + pr, U[2] * w, Hs * vv},
-                               {U[3], U[3] * u, U[3] * vv, U[3] * w + pr, Hs * w}};
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                const T j0 = T(G[(3 * k) * E + ee]), j1 = T(G[(3 * k + 1) * E + ee]), j2 = T(G[(3 * k + 2) * E + ee]);
-#pragma unroll
-                for (int cc = 0; cc < 5; ++cc) sl[k * 5 + cc] = j0 * F[0][cc] + j1 * F[1][cc] + j2 * F[2][cc];
-            }
+            sl[0] = U[1];
+            sl[1] = U[1] * u + pr;
+            sl[2] = U[1] * vv;
+            sl[3] = U[1] * w;
+            sl[4] = Hs * u;
+            sl[5] = U[2];
+            sl[6] = U[2] * u;
+            sl[7] = U[2] * vv + pr;
+            sl[8] = U[2] * w;
+            sl[9] = Hs * vv;
+            sl[10] = U[3];
+            sl[11] = U[3] * u;
+            sl[12] = U[3] * vv;
+            sl[13] = U[3] * w + pr;
+            sl[14] = Hs * w;
         }
         __syncthreads();
-        // phase C (volume)
+        // phase C (volume): contravariant flux of variable v, J^-1 F
         if (live) {
             sfor<nq>([&](auto qq) {
                 const T* sl = X + (qq * E + e) * XS;
-                const T fd[3] = {sl[v], sl[5 + v], sl[10 + v]};
+                const T fx = sl[v], fy = sl[5 + v], fz = sl[10 + v];
+                const T fd[3] = {ji[0] * fx + ji[1] * fy + ji[2] * fz, ji[3] * fx + ji[4] * fy + ji[5] * fz,
+                                 ji[6] * fx + ji[7] * fy + ji[8] * fz};
                 sfor<NB>([&](auto i) {
                     sfor<3>([&](auto d) {
                         if constexpr (expt(i, d) > 0) acc[i] += TAB(VD, T, ((q0 + qq) * NB + i) * 3 + d) * fd[d];
@@ -517,6 +530,7 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? 4 : 3) elem_stage_k
         if (a.combine >= 0) {
             const double dt = a.dt_is_vector ? a.dt[gid] : a.dt[0];
             double mean = 0.0;
+            double outr[NB];
             sfor<NB>([&](auto j) {
                 double u0j = 0.0;
                 if (need_u0) {
@@ -530,9 +544,17 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? 4 : 3) elem_stage_k
                     o = a.b * (c[j] + dt * r[j]);
                     if (a.a != 0.0) o = a.a * u0j + o;
                 }
-                S[e * RS + v * NB + j] = o;
+                outr[j] = o;
                 mean += MEAN_T[j] * o;
             });
+            if constexpr ((NB % 2) == 0) {
+#pragma unroll
+                for (int j = 0; j < NB; j += 2)
+                    *reinterpret_cast<double2*>(S + e * RS + v * NB + j) = make_double2(outr[j], outr[j + 1]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < NB; ++j) S[e * RS + v * NB + j] = outr[j];
+            }
             RED[5 * E + v * E + e] = mean;
         }
     }
