@@ -346,7 +346,7 @@ def run_reference(args):
         "steps": steps,
         "warmup": args.warmup,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64" if args.prec == 64 else "f32",
         "data": "synthetic Kuhn-cube tetrahedral mesh, projected isentropic vortex tube",

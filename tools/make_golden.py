@@ -38,6 +38,7 @@ from hodg import mesh as M  # noqa: E402
 from hodg.config import RunConfig  # noqa: E402
 from hodg.geometry import compute_geometry  # noqa: E402
 from hodg.output import write_residual_csv  # noqa: E402
+from hodg.perf import MachineModel, PerfSample, emit_roofline_csv, emit_timing_csv  # noqa: E402
 from hodg.physics import Conserved, GasModel, boundary_state, roe_flux  # noqa: E402
 from hodg.renumber import AdjacencyGraph, apply_permutation, build_adjacency, export_spy, random_permutation, rcm  # noqa: E402
 from hodg.timestepping import run  # noqa: E402
@@ -73,6 +74,19 @@ def main():
     export_spy(graph, rcm(graph), os.path.join(OUT, "spy_after.mtx"))
     export_spy(AdjacencyGraph.from_edges(3, [(0, 1), (1, 2)]), None, os.path.join(OUT, "spy_path3.mtx"))
     for n in ("spy_before.mtx", "spy_after.mtx", "spy_path3.mtx"):
+        assert open(os.path.join(OUT, n), "rb").read() == open(os.path.join(REF, "fixtures", n), "rb").read()
+
+    # synthetic perf fixtures (pkg/tests/test_fixtures.py:61-78)
+    samples = [
+        ("grid4", PerfSample(wall_seconds=0.020, flops=4.0e8, dram_bytes=3.2e9, iterations=1)),
+        ("grid5", PerfSample(wall_seconds=0.085, flops=1.6e9, dram_bytes=1.28e10, iterations=1)),
+        ("dense", PerfSample(wall_seconds=0.010, flops=5.0e9, dram_bytes=2.0e8, iterations=1)),
+    ]
+    machines = [MachineModel("cpu-node", 3.0e12, 2.0e11), MachineModel("gpu-node", 7.0e12, 9.0e11)]
+    emit_roofline_csv(samples, machines, os.path.join(OUT, "roofline.csv"))
+    emit_timing_csv([("grid4", 1, 0.0400), ("grid4", 2, 0.0215), ("grid4", 8, 0.0095),
+                     ("grid5", 1, 0.1660), ("grid5", 2, 0.0890), ("grid5", 8, 0.0410)], os.path.join(OUT, "timing.csv"))
+    for n in ("roofline.csv", "timing.csv"):
         assert open(os.path.join(OUT, n), "rb").read() == open(os.path.join(REF, "fixtures", n), "rb").read()
 
     # residuals of perturbed freestream / vortex projections on the corpus
