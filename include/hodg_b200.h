@@ -162,6 +162,13 @@ int hodg_rcm(int64_t n, const int64_t* indptr, const int64_t* indices, int64_t* 
  *   hodg2d_dt_pass    <- _dt_pass              hodg/timestepping.py:105-134
  *   hodg2d_axpy       <- _axpy_state           hodg/timestepping.py:165-171
  *   hodg2d_combine    <- _combine_state        hodg/timestepping.py:174-180
+ * and the viscous (ivis = 1, BR1) kernels of the same table:
+ *   hodg2d_qhat_pass     <- qhat_pass            hodg/dg.py:114-162
+ *   hodg2d_aux_pass      <- aux_pass             hodg/dg.py:164-238
+ *   hodg2d_flux_pass_ns  <- flux_pass, ivis = 1  hodg/dg.py:240-351
+ *   hodg2d_rhs_pass_ns   <- rhs_pass, ivis = 1   hodg/dg.py:353-460
+ * (aux is (n_cells, 2, 4, nb) at the state precision, minv of aux_pass too;
+ * the reference's scratch arrays live in registers).
  * Error flags are the reference's uint8 per-face / per-cell arrays. */
 int hodg2d_flux_pass(int prec, int64_t n_faces, int nqf, int nb, const void* coeffs, const void* fbL, const void* fbR,
                      const int32_t* face_cells, const int8_t* bc_code, const void* fnx, const void* fny,
@@ -171,6 +178,24 @@ int hodg2d_rhs_pass(int prec, int64_t n_cells, int nb, int nqv, int nqf, int max
                     const void* vol_gy, const int8_t* cell_nfaces, const int32_t* cell_faces,
                     const int8_t* cell_fsign, const void* face_w, const void* fbL, const void* fbR,
                     const double* minv64, double gamma, double* res, uint8_t* errc, void* stream);
+int hodg2d_qhat_pass(int prec, int64_t n_faces, int nqf, int nb, const void* coeffs, const void* fbL, const void* fbR,
+                     const int32_t* face_cells, const int8_t* bc_code, const void* fnx, const void* fny,
+                     const void* qinf, double gamma, void* qhat, uint8_t* errf, void* stream);
+int hodg2d_aux_pass(int prec, int64_t n_cells, int nb, int nqv, int nqf, int maxf, const void* coeffs,
+                    const void* qhat, const void* vol_w, const void* vol_basis, const void* vol_gx,
+                    const void* vol_gy, const int8_t* cell_nfaces, const int32_t* cell_faces,
+                    const int8_t* cell_fsign, const void* face_w, const void* fbL, const void* fbR, const void* fnx,
+                    const void* fny, const void* minv, void* aux, void* stream);
+int hodg2d_flux_pass_ns(int prec, int64_t n_faces, int nqf, int nb, const void* coeffs, const void* aux,
+                        const void* fbL, const void* fbR, const int32_t* face_cells, const int8_t* bc_code,
+                        const void* fnx, const void* fny, const void* qinf, double gamma, double Rgas, double mu,
+                        double Pr, void* finv, void* fvis, void* fqhat, uint8_t* errf, void* stream);
+int hodg2d_rhs_pass_ns(int prec, int64_t n_cells, int nb, int nqv, int nqf, int maxf, const void* coeffs,
+                       const void* aux, const void* finv, const void* fvis, const void* vol_w, const void* vol_basis,
+                       const void* vol_gx, const void* vol_gy, const int8_t* cell_nfaces, const int32_t* cell_faces,
+                       const int8_t* cell_fsign, const void* face_w, const void* fbL, const void* fbR,
+                       const double* minv64, double gamma, double Rgas, double mu, double Pr, double* res,
+                       uint8_t* errc, void* stream);
 int hodg2d_dt_pass(int prec, int64_t n_cells, int nb, const void* coeffs, const double* basis_mean, const double* h,
                    double gamma, double mu, double cfl, int order, double* out, uint8_t* errc, void* stream);
 int hodg2d_axpy(int prec, int64_t n_cells, int per_cell, const void* u, const double* r, const double* dtc, void* out,

@@ -47,6 +47,11 @@ def lib():
             getattr(_lib, "ora_rk_combo" + sfx).argtypes = [I64, I32, D, D, P, P, P, P, P]
             getattr(_lib, "ora_point_flux" + sfx).argtypes = [I32, I64, P, P, P, D, I32, P, P]
             getattr(_lib, "ora_point_bstate" + sfx).argtypes = [I32, I64, I32, P, P, P, D, P]
+            getattr(_lib, "ora_qhat_pass" + sfx).argtypes = [I64, I32, I32, P, P, P, P, P, P, P, P, D, P, P]
+            getattr(_lib, "ora_aux_pass" + sfx).argtypes = [I64, I32, I32, I32, I32] + [P] * 17
+            getattr(_lib, "ora_flux_pass_ns" + sfx).argtypes = [I64, I32, I32] + [P] * 9 + [D] * 4 + [P] * 4
+            getattr(_lib, "ora_rhs_pass_ns" + sfx).argtypes = [I64, I32, I32, I32, I32] + [P] * 15 + [D] * 4 + \
+                [P] * 3
         _lib.ora_set_threads.argtypes = [I32]
         _lib.ora_set_threads.restype = I32
     return _lib

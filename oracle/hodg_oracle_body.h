@@ -223,6 +223,300 @@ static void CAT(bstate, SFX)(int kind, const REAL *q, const REAL *n, const REAL 
     }
 }
 
+/* ---- viscous (BR1) terms, 2D: hodg/physics.py:252-290, hodg/dg.py:114-238 ---- */
+
+/* hodg/physics.py:252-269 */
+static inline void CAT(vel_temp_grads, SFX)(REAL rho, REAL ru, REAL rv, REAL e, const REAL *zx, const REAL *zy,
+                                            REAL gamma, REAL Rgas, REAL *out8) {
+    REAL u = ru / rho;
+    REAL v = rv / rho;
+    REAL ux = (zx[1] - u * zx[0]) / rho;
+    REAL vx = (zx[2] - v * zx[0]) / rho;
+    REAL uy = (zy[1] - u * zy[0]) / rho;
+    REAL vy = (zy[2] - v * zy[0]) / rho;
+    REAL ke = HALF * (u * u + v * v);
+    REAL ein = e - rho * ke;
+    REAL kx = ke * zx[0] + rho * (u * ux + v * vx);
+    REAL ky = ke * zy[0] + rho * (u * uy + v * vy);
+    REAL coef = (gamma - ONE) / Rgas;
+    REAL Tx = coef * ((zx[3] - kx) * rho - ein * zx[0]) / (rho * rho);
+    REAL Ty = coef * ((zy[3] - ky) * rho - ein * zy[0]) / (rho * rho);
+    out8[0] = u; out8[1] = v; out8[2] = ux; out8[3] = uy; out8[4] = vx; out8[5] = vy; out8[6] = Tx; out8[7] = Ty;
+}
+
+/* hodg/physics.py:271-277; returns txx, txy, tyy, qx, qy */
+static inline void CAT(stress_heat, SFX)(REAL ux, REAL uy, REAL vx, REAL vy, REAL Tx, REAL Ty, REAL gamma,
+                                         REAL Rgas, REAL mu, REAL Pr, REAL *o5) {
+    const REAL two_thirds = (REAL)(2.0 / 3.0);
+    o5[0] = mu * two_thirds * (TWO * ux - vy);
+    o5[2] = mu * two_thirds * (TWO * vy - ux);
+    o5[1] = mu * (uy + vx);
+    REAL k = mu * gamma * Rgas / ((gamma - ONE) * Pr);
+    o5[3] = -k * Tx;
+    o5[4] = -k * Ty;
+}
+
+/* hodg/physics.py:279-290 */
+static inline void CAT(viscn, SFX)(REAL rho, REAL ru, REAL rv, REAL e, const REAL *zx, const REAL *zy, REAL nx,
+                                   REAL ny, REAL gamma, REAL Rgas, REAL mu, REAL Pr, REAL *h) {
+    REAL g8[8], s5[5];
+    CAT(vel_temp_grads, SFX)(rho, ru, rv, e, zx, zy, gamma, Rgas, g8);
+    CAT(stress_heat, SFX)(g8[2], g8[3], g8[4], g8[5], g8[6], g8[7], gamma, Rgas, mu, Pr, s5);
+    REAL u = g8[0], v = g8[1];
+    h[0] = ZERO;
+    h[1] = s5[0] * nx + s5[1] * ny;
+    h[2] = s5[1] * nx + s5[2] * ny;
+    h[3] = (u * s5[0] + v * s5[1] - s5[3]) * nx + (u * s5[1] + v * s5[2] - s5[4]) * ny;
+}
+
+/* hodg/dg.py:114-162 (qhat_pass): central trace average; 2D */
+void CAT(ora_qhat_pass, SFX)(int64_t n_faces, int nqf, int nb, const REAL *coeffs, const REAL *fbL, const REAL *fbR,
+                             const int32_t *face_cells, const int8_t *bc_code, const REAL *fnx, const REAL *fny,
+                             const REAL *qinf, double gamma, REAL *qhat, uint8_t *errf) {
+    const int d3 = 0;
+    const REAL g = (REAL)gamma;
+#pragma omp parallel for schedule(static)
+    for (int64_t f = 0; f < n_faces; ++f) {
+        int64_t iL = face_cells[2 * f], iR = face_cells[2 * f + 1];
+        REAL n[2] = {fnx[f], fny[f]};
+        for (int q = 0; q < nqf; ++q) {
+            REAL qL[4] = {ZERO, ZERO, ZERO, ZERO}, qR[4] = {ZERO, ZERO, ZERO, ZERO};
+            for (int k = 0; k < nb; ++k) {
+                REAL b = fbL[(f * nqf + q) * nb + k];
+                for (int v = 0; v < 4; ++v) qL[v] += b * coeffs[(iL * 4 + v) * nb + k];
+            }
+            if (iR >= 0) {
+                for (int k = 0; k < nb; ++k) {
+                    REAL b = fbR[(f * nqf + q) * nb + k];
+                    for (int v = 0; v < 4; ++v) qR[v] += b * coeffs[(iR * 4 + v) * nb + k];
+                }
+            } else {
+                if (qL[0] <= ZERO) {
+                    errf[f] = 1;
+                    continue;
+                }
+                REAL u, v, w;
+                REAL pL = CAT(prim_p, SFX)(qL[0], qL[1], qL[2], ZERO, qL[3], g, d3, &u, &v, &w);
+                if (pL <= ZERO) {
+                    errf[f] = 1;
+                    continue;
+                }
+                CAT(bstate, SFX)(bc_code[f], qL, n, qinf, g, d3, qR);
+            }
+            for (int v = 0; v < 4; ++v) qhat[(f * nqf + q) * 4 + v] = HALF * (qL[v] + qR[v]);
+        }
+    }
+}
+
+/* hodg/dg.py:164-238 (aux_pass): weak gradient z = M^-1 [-int Q grad b + sum qhat n b] (2D).
+ * aux is (N, 2, 4, nb); scratch (N, 2, 4, nb); minv at REAL precision */
+void CAT(ora_aux_pass, SFX)(int64_t n_cells, int nb, int nqv, int nqf, int maxf, const REAL *coeffs,
+                            const REAL *qhat, const REAL *vol_w, const REAL *vol_basis, const REAL *vol_gx,
+                            const REAL *vol_gy, const int8_t *cell_nfaces, const int32_t *cell_faces,
+                            const int8_t *cell_fsign, const REAL *face_w, const REAL *fbL, const REAL *fbR,
+                            const REAL *fnx, const REAL *fny, const REAL *minv, REAL *scratch, REAL *aux) {
+#pragma omp parallel for schedule(static)
+    for (int64_t c = 0; c < n_cells; ++c) {
+        REAL *sc = scratch + c * 8 * nb;
+        for (int i = 0; i < 8 * nb; ++i) sc[i] = ZERO;
+        const REAL *cc = coeffs + c * 4 * nb;
+        for (int qp = 0; qp < nqv; ++qp) {
+            REAL w = vol_w[c * nqv + qp];
+            if (w == ZERO) continue;
+            REAL qv[4] = {ZERO, ZERO, ZERO, ZERO};
+            for (int k = 0; k < nb; ++k) {
+                REAL b = vol_basis[(c * nqv + qp) * nb + k];
+                for (int v = 0; v < 4; ++v) qv[v] += b * cc[v * nb + k];
+            }
+            for (int j = 0; j < nb; ++j) {
+                REAL gx = w * vol_gx[(c * nqv + qp) * nb + j];
+                REAL gy = w * vol_gy[(c * nqv + qp) * nb + j];
+                for (int v = 0; v < 4; ++v) sc[(0 * 4 + v) * nb + j] -= qv[v] * gx;
+                for (int v = 0; v < 4; ++v) sc[(1 * 4 + v) * nb + j] -= qv[v] * gy;
+            }
+        }
+        for (int slot = 0; slot < cell_nfaces[c]; ++slot) {
+            int64_t fid = cell_faces[c * maxf + slot];
+            int sgn = cell_fsign[c * maxf + slot];
+            const REAL *tb = sgn > 0 ? fbL : fbR;
+            REAL s = (REAL)sgn;
+            REAL nx = fnx[fid], ny = fny[fid];
+            for (int q = 0; q < nqf; ++q) {
+                REAL w = s * face_w[fid * nqf + q];
+                const REAL *h = qhat + (fid * nqf + q) * 4;
+                REAL wx = w * nx;
+                REAL wy = w * ny;
+                for (int j = 0; j < nb; ++j) {
+                    REAL b = tb[(fid * nqf + q) * nb + j];
+                    for (int v = 0; v < 4; ++v) sc[(0 * 4 + v) * nb + j] += h[v] * wx * b;
+                    for (int v = 0; v < 4; ++v) sc[(1 * 4 + v) * nb + j] += h[v] * wy * b;
+                }
+            }
+        }
+        const REAL *mi = minv + c * nb * nb;
+        for (int d = 0; d < 2; ++d)
+            for (int v = 0; v < 4; ++v)
+                for (int j = 0; j < nb; ++j) {
+                    REAL acc = ZERO;
+                    for (int k = 0; k < nb; ++k) acc += mi[j * nb + k] * sc[(d * 4 + v) * nb + k];
+                    aux[((c * 2 + d) * 4 + v) * nb + j] = acc;
+                }
+    }
+}
+
+/* hodg/dg.py:240-351 with ivis = 1 (2D): Roe flux plus the central viscous
+ * flux fvis and the trace average fqhat */
+void CAT(ora_flux_pass_ns, SFX)(int64_t n_faces, int nqf, int nb, const REAL *coeffs, const REAL *aux, const REAL *fbL,
+                                const REAL *fbR, const int32_t *face_cells, const int8_t *bc_code, const REAL *fnx,
+                                const REAL *fny, const REAL *qinf, double gamma, double Rgas, double mu, double Pr,
+                                REAL *finv, REAL *fvis, REAL *fqhat, uint8_t *errf) {
+    const int d3 = 0;
+    const REAL g = (REAL)gamma, R = (REAL)Rgas, m = (REAL)mu, pr = (REAL)Pr;
+#pragma omp parallel for schedule(static)
+    for (int64_t f = 0; f < n_faces; ++f) {
+        int64_t iL = face_cells[2 * f], iR = face_cells[2 * f + 1];
+        REAL n[2] = {fnx[f], fny[f]};
+        for (int q = 0; q < nqf; ++q) {
+            REAL qL[4] = {ZERO, ZERO, ZERO, ZERO}, qR[4] = {ZERO, ZERO, ZERO, ZERO};
+            REAL zLx[4] = {ZERO, ZERO, ZERO, ZERO}, zLy[4] = {ZERO, ZERO, ZERO, ZERO};
+            for (int k = 0; k < nb; ++k) {
+                REAL b = fbL[(f * nqf + q) * nb + k];
+                for (int v = 0; v < 4; ++v) qL[v] += b * coeffs[(iL * 4 + v) * nb + k];
+            }
+            for (int k = 0; k < nb; ++k) {
+                REAL b = fbL[(f * nqf + q) * nb + k];
+                for (int v = 0; v < 4; ++v) zLx[v] += b * aux[((iL * 2 + 0) * 4 + v) * nb + k];
+                for (int v = 0; v < 4; ++v) zLy[v] += b * aux[((iL * 2 + 1) * 4 + v) * nb + k];
+            }
+            REAL zRx[4], zRy[4];
+            for (int v = 0; v < 4; ++v) {
+                zRx[v] = zLx[v];
+                zRy[v] = zLy[v];
+            }
+            if (iR >= 0) {
+                for (int k = 0; k < nb; ++k) {
+                    REAL b = fbR[(f * nqf + q) * nb + k];
+                    for (int v = 0; v < 4; ++v) qR[v] += b * coeffs[(iR * 4 + v) * nb + k];
+                }
+                for (int v = 0; v < 4; ++v) zRx[v] = zRy[v] = ZERO;
+                for (int k = 0; k < nb; ++k) {
+                    REAL b = fbR[(f * nqf + q) * nb + k];
+                    for (int v = 0; v < 4; ++v) zRx[v] += b * aux[((iR * 2 + 0) * 4 + v) * nb + k];
+                    for (int v = 0; v < 4; ++v) zRy[v] += b * aux[((iR * 2 + 1) * 4 + v) * nb + k];
+                }
+            } else {
+                if (qL[0] <= ZERO) {
+                    errf[f] = 1;
+                    continue;
+                }
+                REAL u, v, w;
+                REAL pL = CAT(prim_p, SFX)(qL[0], qL[1], qL[2], ZERO, qL[3], g, d3, &u, &v, &w);
+                if (pL <= ZERO) {
+                    errf[f] = 1;
+                    continue;
+                }
+                CAT(bstate, SFX)(bc_code[f], qL, n, qinf, g, d3, qR);
+            }
+            REAL h[4];
+            if (!CAT(roe, SFX)(qL, qR, n, g, d3, h)) {
+                errf[f] = 1;
+                continue;
+            }
+            for (int v = 0; v < 4; ++v) finv[(f * nqf + q) * 4 + v] = h[v];
+            REAL hL[4], hR[4];
+            CAT(viscn, SFX)(qL[0], qL[1], qL[2], qL[3], zLx, zLy, n[0], n[1], g, R, m, pr, hL);
+            CAT(viscn, SFX)(qR[0], qR[1], qR[2], qR[3], zRx, zRy, n[0], n[1], g, R, m, pr, hR);
+            for (int v = 0; v < 4; ++v) {
+                fvis[(f * nqf + q) * 4 + v] = HALF * (hL[v] + hR[v]);
+                fqhat[(f * nqf + q) * 4 + v] = HALF * (qL[v] + qR[v]);
+            }
+        }
+    }
+}
+
+/* hodg/dg.py:353-460 with ivis = 1 (2D) */
+void CAT(ora_rhs_pass_ns, SFX)(int64_t n_cells, int nb, int nqv, int nqf, int maxf, const REAL *coeffs,
+                               const REAL *aux, const REAL *finv, const REAL *fvis, const REAL *vol_w,
+                               const REAL *vol_basis, const REAL *vol_gx, const REAL *vol_gy,
+                               const int8_t *cell_nfaces, const int32_t *cell_faces, const int8_t *cell_fsign,
+                               const REAL *face_w, const REAL *fbL, const REAL *fbR, const double *minv64,
+                               double gamma, double Rgas, double mu, double Pr, double *scratch, double *res,
+                               uint8_t *errc) {
+    const int d3 = 0;
+    const REAL g = (REAL)gamma, R = (REAL)Rgas, m = (REAL)mu, pr = (REAL)Pr;
+#pragma omp parallel for schedule(static)
+    for (int64_t c = 0; c < n_cells; ++c) {
+        double *sc = scratch + c * 4 * nb;
+        for (int i = 0; i < 4 * nb; ++i) sc[i] = 0.0;
+        const REAL *cc = coeffs + c * 4 * nb;
+        for (int qp = 0; qp < nqv; ++qp) {
+            REAL w = vol_w[c * nqv + qp];
+            if (w == ZERO) continue;
+            REAL qv[4] = {ZERO, ZERO, ZERO, ZERO};
+            for (int k = 0; k < nb; ++k) {
+                REAL b = vol_basis[(c * nqv + qp) * nb + k];
+                for (int v = 0; v < 4; ++v) qv[v] += b * cc[v * nb + k];
+            }
+            if (qv[0] <= ZERO) {
+                errc[c] = 1;
+                continue;
+            }
+            REAL u, v_, wz;
+            REAL p = CAT(prim_p, SFX)(qv[0], qv[1], qv[2], ZERO, qv[3], g, d3, &u, &v_, &wz);
+            if (p <= ZERO) {
+                errc[c] = 1;
+                continue;
+            }
+            REAL ex[4] = {qv[1], qv[1] * u + p, qv[1] * v_, (qv[3] + p) * u};
+            REAL fy[4] = {qv[2], qv[2] * u, qv[2] * v_ + p, (qv[3] + p) * v_};
+            REAL zx[4] = {ZERO, ZERO, ZERO, ZERO}, zy[4] = {ZERO, ZERO, ZERO, ZERO};
+            for (int k = 0; k < nb; ++k) {
+                REAL b = vol_basis[(c * nqv + qp) * nb + k];
+                for (int vv = 0; vv < 4; ++vv) zx[vv] += b * aux[((c * 2 + 0) * 4 + vv) * nb + k];
+                for (int vv = 0; vv < 4; ++vv) zy[vv] += b * aux[((c * 2 + 1) * 4 + vv) * nb + k];
+            }
+            REAL g8[8], s5[5];
+            CAT(vel_temp_grads, SFX)(qv[0], qv[1], qv[2], qv[3], zx, zy, g, R, g8);
+            CAT(stress_heat, SFX)(g8[2], g8[3], g8[4], g8[5], g8[6], g8[7], g, R, m, pr, s5);
+            REAL uu = g8[0], vv2 = g8[1];
+            ex[1] -= s5[0];
+            ex[2] -= s5[1];
+            ex[3] -= uu * s5[0] + vv2 * s5[1] - s5[3];
+            fy[1] -= s5[1];
+            fy[2] -= s5[2];
+            fy[3] -= uu * s5[1] + vv2 * s5[2] - s5[4];
+            for (int j = 0; j < nb; ++j) {
+                REAL gx = w * vol_gx[(c * nqv + qp) * nb + j];
+                REAL gy = w * vol_gy[(c * nqv + qp) * nb + j];
+                for (int vv = 0; vv < 4; ++vv) sc[vv * nb + j] += ex[vv] * gx + fy[vv] * gy;
+            }
+        }
+        for (int slot = 0; slot < cell_nfaces[c]; ++slot) {
+            int64_t fid = cell_faces[c * maxf + slot];
+            int sgn = cell_fsign[c * maxf + slot];
+            const REAL *tb = sgn > 0 ? fbL : fbR;
+            REAL s = (REAL)sgn;
+            for (int q = 0; q < nqf; ++q) {
+                REAL w = s * face_w[fid * nqf + q];
+                REAL h[4];
+                for (int vv = 0; vv < 4; ++vv) h[vv] = finv[(fid * nqf + q) * 4 + vv];
+                for (int vv = 0; vv < 4; ++vv) h[vv] -= fvis[(fid * nqf + q) * 4 + vv];
+                for (int j = 0; j < nb; ++j) {
+                    REAL wb = w * tb[(fid * nqf + q) * nb + j];
+                    for (int vv = 0; vv < 4; ++vv) sc[vv * nb + j] -= h[vv] * wb;
+                }
+            }
+        }
+        const double *mi = minv64 + c * nb * nb;
+        for (int vv = 0; vv < 4; ++vv)
+            for (int j = 0; j < nb; ++j) {
+                double acc = 0.0;
+                for (int k = 0; k < nb; ++k) acc += mi[j * nb + k] * sc[vv * nb + k];
+                res[(c * 4 + vv) * nb + j] = acc;
+            }
+    }
+}
+
 /* Batched point evaluations of the interface flux and the boundary state
  * (the reference's Python API roe_flux / boundary_state,
  * hodg/physics.py:436-479).  q arrays are (n, nv), normals (n, dim). */

@@ -46,6 +46,8 @@ class Gas:
     gamma: float = 1.4
     R: float = 1.0
     mu: float = 0.0
+    Pr: float = 0.72
+    ivis: int = 0  # 1: Navier-Stokes with BR1 viscous terms (2D; hodg/physics.py:76-100)
 
 
 # ---------------------------------------------------------------------------
@@ -90,6 +92,24 @@ def vortex_primitive(gas, mach, angle_deg, beta, x0, y0, t, x, y, dim=2):
     p = rho * gas.R * T
     if dim == 3:
         return rho, u, v, np.zeros_like(u), p
+    return rho, u, v, p
+
+
+def pulse_primitive(gas, amplitude, sigma, x0, y0, x, y, mach=0.0, angle_deg=0.0, dim=2):
+    """hodg/flows.py:60-73; in 3D a tube along z (w = 0)."""
+    x = np.asarray(x, dtype=np.float64)
+    y = np.asarray(y, dtype=np.float64)
+    r2 = (x - x0) ** 2 + (y - y0) ** 2
+    p_inf = gas.R
+    p = p_inf * (1.0 + amplitude * np.exp(-0.5 * r2 / (sigma * sigma)))
+    rho = (p / p_inf) ** (1.0 / gas.gamma)
+    if mach > 0.0:
+        inf = freestream_primitive(gas, mach, angle_deg, 2)
+        u, v = np.full_like(p, inf[1]), np.full_like(p, inf[2])
+    else:
+        u, v = np.zeros_like(p), np.zeros_like(p)
+    if dim == 3:
+        return rho, u, v, np.zeros_like(p), p
     return rho, u, v, p
 
 
@@ -172,8 +192,85 @@ class Disc:
             raise AdmissibilityError("inadmissible volume state", cell=int(np.nonzero(errc)[0][0]), iteration=iteration)
         return res
 
+    # -- viscous (BR1) terms, hodg/dg.py:572-663 ---------------------------
+    def _check_2d_viscous(self):
+        if self.mesh.dim != 2:
+            raise NotImplementedError("the oracle's viscous terms follow the reference and are 2D")
+
+    def aux_gradient(self, coeffs, iteration=None):
+        """compute_aux_gradient (hodg/dg.py:572-591): qhat_pass then aux_pass."""
+        self._check_2d_viscous()
+        m, t = self.mesh, self.tab
+        b = self.bundle(coeffs.dtype)
+        L, sf = _clib.lib(), _clib.sfx(coeffs.dtype)
+        nqf, nb = t.n_face_points, t.n_basis
+        qhat = np.zeros((m.n_faces, nqf, 4), dtype=coeffs.dtype)
+        errf = np.zeros(m.n_faces, dtype=np.uint8)
+        nrm = b["normal"]
+        getattr(L, "ora_qhat_pass" + sf)(
+            m.n_faces, nqf, nb, _clib.ptr(coeffs), _clib.ptr(b["face_basis_l"]), _clib.ptr(b["face_basis_r"]),
+            _clib.ptr(m.face_cells), _clib.ptr(self.bc), _clib.ptr(nrm[0]), _clib.ptr(nrm[1]), _clib.ptr(b["qinf"]),
+            self.gas.gamma, _clib.ptr(qhat), _clib.ptr(errf))
+        if errf.any():
+            raise AdmissibilityError("inadmissible face trace", face=int(np.nonzero(errf)[0][0]), iteration=iteration)
+        aux = np.empty((m.n_cells, 2, 4, nb), dtype=coeffs.dtype)
+        scratch = np.zeros_like(aux)
+        minv = b.get("minv_cast")
+        if minv is None:
+            minv = b["minv_cast"] = np.ascontiguousarray(t.minv, dtype=coeffs.dtype)
+        g = b["vol_grad"]
+        getattr(L, "ora_aux_pass" + sf)(
+            m.n_cells, nb, t.n_vol_points, nqf, m.cell_faces.shape[1], _clib.ptr(coeffs), _clib.ptr(qhat),
+            _clib.ptr(b["vol_w"]), _clib.ptr(b["vol_basis"]), _clib.ptr(g[0]), _clib.ptr(g[1]),
+            _clib.ptr(m.cell_nfaces), _clib.ptr(m.cell_faces), _clib.ptr(m.cell_fsign), _clib.ptr(b["face_w"]),
+            _clib.ptr(b["face_basis_l"]), _clib.ptr(b["face_basis_r"]), _clib.ptr(nrm[0]), _clib.ptr(nrm[1]),
+            _clib.ptr(minv), _clib.ptr(scratch), _clib.ptr(aux))
+        return aux
+
+    def flux_pass_ns(self, coeffs, aux, iteration=None):
+        """flux_pass with ivis = 1 (hodg/dg.py:240-351): (finv, fvis, fqhat)."""
+        self._check_2d_viscous()
+        m, t, gs = self.mesh, self.tab, self.gas
+        b = self.bundle(coeffs.dtype)
+        shp = (m.n_faces, t.n_face_points, 4)
+        finv, fvis, fqhat = (np.zeros(shp, dtype=coeffs.dtype) for _ in range(3))
+        errf = np.zeros(m.n_faces, dtype=np.uint8)
+        nrm = b["normal"]
+        getattr(_clib.lib(), "ora_flux_pass_ns" + _clib.sfx(coeffs.dtype))(
+            m.n_faces, t.n_face_points, t.n_basis, _clib.ptr(coeffs), _clib.ptr(aux), _clib.ptr(b["face_basis_l"]),
+            _clib.ptr(b["face_basis_r"]), _clib.ptr(m.face_cells), _clib.ptr(self.bc), _clib.ptr(nrm[0]),
+            _clib.ptr(nrm[1]), _clib.ptr(b["qinf"]), gs.gamma, gs.R, gs.mu, gs.Pr, _clib.ptr(finv), _clib.ptr(fvis),
+            _clib.ptr(fqhat), _clib.ptr(errf))
+        if errf.any():
+            raise AdmissibilityError("inadmissible face trace", face=int(np.nonzero(errf)[0][0]), iteration=iteration)
+        return finv, fvis, fqhat
+
+    def rhs_pass_ns(self, coeffs, aux, finv, fvis, iteration=None):
+        """rhs_pass with ivis = 1 (hodg/dg.py:353-460)."""
+        self._check_2d_viscous()
+        m, t, gs = self.mesh, self.tab, self.gas
+        b = self.bundle(coeffs.dtype)
+        res = np.empty((m.n_cells, 4, t.n_basis))
+        scratch = np.zeros_like(res)
+        errc = np.zeros(m.n_cells, dtype=np.uint8)
+        g = b["vol_grad"]
+        getattr(_clib.lib(), "ora_rhs_pass_ns" + _clib.sfx(coeffs.dtype))(
+            m.n_cells, t.n_basis, t.n_vol_points, t.n_face_points, m.cell_faces.shape[1], _clib.ptr(coeffs),
+            _clib.ptr(aux), _clib.ptr(finv), _clib.ptr(fvis), _clib.ptr(b["vol_w"]), _clib.ptr(b["vol_basis"]),
+            _clib.ptr(g[0]), _clib.ptr(g[1]), _clib.ptr(m.cell_nfaces), _clib.ptr(m.cell_faces),
+            _clib.ptr(m.cell_fsign), _clib.ptr(b["face_w"]), _clib.ptr(b["face_basis_l"]),
+            _clib.ptr(b["face_basis_r"]), _clib.ptr(t.minv), gs.gamma, gs.R, gs.mu, gs.Pr, _clib.ptr(scratch),
+            _clib.ptr(res), _clib.ptr(errc))
+        if errc.any():
+            raise AdmissibilityError("inadmissible volume state", cell=int(np.nonzero(errc)[0][0]), iteration=iteration)
+        return res
+
     def rhs(self, coeffs, iteration=None):
         coeffs = np.ascontiguousarray(coeffs)
+        if self.gas.ivis:
+            aux = self.aux_gradient(coeffs, iteration)
+            finv, fvis, _ = self.flux_pass_ns(coeffs, aux, iteration)
+            return self.rhs_pass_ns(coeffs, aux, finv, fvis, iteration)
         return self.rhs_pass(coeffs, self.flux_pass(coeffs, iteration), iteration)
 
 
@@ -302,8 +399,10 @@ class RunSpec:
     gas: Gas = Gas()
     mach: float = 0.3
     angle_deg: float = 0.0
-    initial: str = "freestream"  # freestream | vortex
+    initial: str = "freestream"  # freestream | vortex | pulse
     beta: float = 5.0
+    amplitude: float = 0.2
+    sigma: float = 0.1
     x0: float = 0.0
     y0: float = 0.0
     cfl: float = 0.3
@@ -331,6 +430,10 @@ def initial_state(spec, disc):
         def fld(*xs):
             return vortex_primitive(gas, spec.mach, spec.angle_deg, spec.beta, spec.x0, spec.y0, 0.0, xs[0], xs[1],
                                     dim=m.dim)
+    elif spec.initial == "pulse":
+        def fld(*xs):
+            return pulse_primitive(gas, spec.amplitude, spec.sigma, spec.x0, spec.y0, xs[0], xs[1], spec.mach,
+                                   spec.angle_deg, dim=m.dim)
     else:
         w = freestream_primitive(gas, spec.mach, spec.angle_deg, m.dim)
 

@@ -94,6 +94,10 @@ SIGNATURES = {
     "hodg_face_sort": (I32, [I64, I64, P, P, P, P]),
     "hodg2d_flux_pass": (I32, [I32, I64, I32, I32, P, P, P, P, P, P, P, P, D, I32, P, P, P]),
     "hodg2d_rhs_pass": (I32, [I32, I64, I32, I32, I32, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, D, P, P, P]),
+    "hodg2d_qhat_pass": (I32, [I32, I64, I32, I32, P, P, P, P, P, P, P, P, D, P, P, P]),
+    "hodg2d_aux_pass": (I32, [I32, I64, I32, I32, I32, I32] + [P] * 17),
+    "hodg2d_flux_pass_ns": (I32, [I32, I64, I32, I32] + [P] * 9 + [D] * 4 + [P] * 5),
+    "hodg2d_rhs_pass_ns": (I32, [I32, I64, I32, I32, I32, I32] + [P] * 15 + [D] * 4 + [P] * 3),
     "hodg2d_dt_pass": (I32, [I32, I64, I32, P, P, P, D, D, D, I32, P, P, P]),
     "hodg2d_axpy": (I32, [I32, I64, I32, P, P, P, P, P]),
     "hodg2d_combine": (I32, [I32, I64, I32, P, P, P, P, P, P]),

@@ -16,6 +16,8 @@
 #include "../../include/hodg_b200.h"
 #include <cuda_runtime.h>
 
+extern int64_t hodg_count_launch(int64_t n);
+
 namespace {
 
 template <typename T>
@@ -100,6 +102,13 @@ __device__ bool llf2(const T* qL, const T* qR, T nx, T ny, T g, T* f) {
     return true;
 }
 
+// x ** y as the reference evaluates it (glibc pow / powf): in FP32 through
+// double precision, which rounds to glibc's (correctly rounded) powf except
+// in astronomically rare near-tie cases; CUDA's own powf is off by an ulp
+// often enough to desynchronise the FP32 fixture histories
+__device__ __forceinline__ double ref_pow(double x, double y) { return pow(x, y); }
+__device__ __forceinline__ float ref_pow(float x, float y) { return float(pow(double(x), double(y))); }
+
 // hodg/physics.py:292-344
 template <typename T>
 __device__ void bstate2(int kind, const T* q, T nx, T ny, const T* qf, T g, T* out) {
@@ -132,15 +141,15 @@ __device__ void bstate2(int kind, const T* q, T nx, T ny, const T* qf, T g, T* o
         }
         T s, utx, uty;
         if (unb > zero) {
-            s = pi / pow(rho, g);
+            s = pi / ref_pow(rho, g);
             utx = ui - uni * nx;
             uty = vi - uni * ny;
         } else {
-            s = pf / pow(rf, g);
+            s = pf / ref_pow(rf, g);
             utx = uf - unf * nx;
             uty = vf - unf * ny;
         }
-        const T rb = pow(ab * ab / (g * s), one / (g - one));
+        const T rb = ref_pow(ab * ab / (g * s), one / (g - one));
         const T pb = rb * ab * ab / g;
         const T ub = utx + unb * nx;
         const T vb = uty + unb * ny;
@@ -162,16 +171,167 @@ __device__ void bstate2(int kind, const T* q, T nx, T ny, const T* qf, T g, T* o
     }
 }
 
-// hodg/dg.py:240-351 (Euler branch): thread per face
+// hodg/physics.py:252-269 -> (u, v, ux, uy, vx, vy, Tx, Ty)
 template <typename T>
-__global__ void flux_pass2d(int64_t n_faces, int nqf, int nb, const T* __restrict__ coeffs, const T* __restrict__ fbL,
+__device__ __forceinline__ void vel_temp_grads2(T rho, T ru, T rv, T e, const T* zx, const T* zy, T g, T R, T* o) {
+    const T u = ru / rho;
+    const T v = rv / rho;
+    const T ux = (zx[1] - u * zx[0]) / rho;
+    const T vx = (zx[2] - v * zx[0]) / rho;
+    const T uy = (zy[1] - u * zy[0]) / rho;
+    const T vy = (zy[2] - v * zy[0]) / rho;
+    const T ke = C2<T>::half * (u * u + v * v);
+    const T ein = e - rho * ke;
+    const T kx = ke * zx[0] + rho * (u * ux + v * vx);
+    const T ky = ke * zy[0] + rho * (u * uy + v * vy);
+    const T coef = (g - C2<T>::one) / R;
+    o[0] = u;
+    o[1] = v;
+    o[2] = ux;
+    o[3] = uy;
+    o[4] = vx;
+    o[5] = vy;
+    o[6] = coef * ((zx[3] - kx) * rho - ein * zx[0]) / (rho * rho);
+    o[7] = coef * ((zy[3] - ky) * rho - ein * zy[0]) / (rho * rho);
+}
+
+// hodg/physics.py:271-277 -> (txx, txy, tyy, qx, qy)
+template <typename T>
+__device__ __forceinline__ void stress_heat2(const T* gr, T g, T R, T mu, T Pr, T* s) {
+    const T two_thirds = T(2.0 / 3.0);
+    const T ux = gr[2], uy = gr[3], vx = gr[4], vy = gr[5];
+    s[0] = mu * two_thirds * (C2<T>::two * ux - vy);
+    s[2] = mu * two_thirds * (C2<T>::two * vy - ux);
+    s[1] = mu * (uy + vx);
+    const T k = mu * g * R / ((g - C2<T>::one) * Pr);
+    s[3] = -k * gr[6];
+    s[4] = -k * gr[7];
+}
+
+// hodg/physics.py:279-290
+template <typename T>
+__device__ __forceinline__ void viscn2(const T* q, const T* zx, const T* zy, T nx, T ny, T g, T R, T mu, T Pr,
+                                       T* h) {
+    T gr[8], s[5];
+    vel_temp_grads2(q[0], q[1], q[2], q[3], zx, zy, g, R, gr);
+    stress_heat2(gr, g, R, mu, Pr, s);
+    const T u = gr[0], v = gr[1];
+    h[0] = C2<T>::zero;
+    h[1] = s[0] * nx + s[1] * ny;
+    h[2] = s[1] * nx + s[2] * ny;
+    h[3] = (u * s[0] + v * s[1] - s[3]) * nx + (u * s[1] + v * s[2] - s[4]) * ny;
+}
+
+// trace of the 4 variables of `src` (cell-major (.., 4, nb)) at one point
+template <typename T>
+__device__ __forceinline__ void trace4(const T* __restrict__ b, const T* __restrict__ src, int nb, T* out) {
+    for (int v = 0; v < 4; ++v) out[v] = C2<T>::zero;
+    for (int k = 0; k < nb; ++k) {
+        const T bk = b[k];
+        for (int v = 0; v < 4; ++v) out[v] += bk * src[v * nb + k];
+    }
+}
+
+// hodg/dg.py:114-162 (qhat_pass): thread per face
+template <typename T>
+__global__ void qhat_pass2d(int64_t n_faces, int nqf, int nb, const T* __restrict__ coeffs, const T* __restrict__ fbL,
                             const T* __restrict__ fbR, const int32_t* __restrict__ face_cells,
                             const int8_t* __restrict__ bc_code, const T* __restrict__ fnx, const T* __restrict__ fny,
-                            const T* __restrict__ qinf, double gamma, int flux_kind, T* __restrict__ finv,
+                            const T* __restrict__ qinf, double gamma, T* __restrict__ qhat,
                             uint8_t* __restrict__ errf) {
     const int64_t f = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (f >= n_faces) return;
     const T g = T(gamma);
+    const int64_t iL = face_cells[2 * f], iR = face_cells[2 * f + 1];
+    const T nx = fnx[f], ny = fny[f];
+    for (int q = 0; q < nqf; ++q) {
+        T qL[4], qR[4];
+        trace4(fbL + (f * nqf + q) * nb, coeffs + iL * 4 * nb, nb, qL);
+        if (iR >= 0) {
+            trace4(fbR + (f * nqf + q) * nb, coeffs + iR * 4 * nb, nb, qR);
+        } else {
+            if (qL[0] <= C2<T>::zero) {
+                errf[f] = 1;
+                continue;
+            }
+            T u, v;
+            if (prim2(qL[0], qL[1], qL[2], qL[3], g, u, v) <= C2<T>::zero) {
+                errf[f] = 1;
+                continue;
+            }
+            const T qf[4] = {qinf[0], qinf[1], qinf[2], qinf[3]};
+            bstate2(bc_code[f], qL, nx, ny, qf, g, qR);
+        }
+        for (int v = 0; v < 4; ++v) qhat[(f * nqf + q) * 4 + v] = C2<T>::half * (qL[v] + qR[v]);
+    }
+}
+
+// hodg/dg.py:164-238 (aux_pass): BR1 weak gradient, thread per cell,
+// accumulated and solved at T as the reference's scratch / minv
+template <typename T>
+__global__ void aux_pass2d(int64_t n_cells, int nb, int nqv, int nqf, int maxf, const T* __restrict__ coeffs,
+                           const T* __restrict__ qhat, const T* __restrict__ vol_w, const T* __restrict__ vol_basis,
+                           const T* __restrict__ vol_gx, const T* __restrict__ vol_gy,
+                           const int8_t* __restrict__ cell_nfaces, const int32_t* __restrict__ cell_faces,
+                           const int8_t* __restrict__ cell_fsign, const T* __restrict__ face_w,
+                           const T* __restrict__ fbL, const T* __restrict__ fbR, const T* __restrict__ fnx,
+                           const T* __restrict__ fny, const T* __restrict__ minv, T* __restrict__ aux) {
+    const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (c >= n_cells) return;
+    T sc[2 * 4 * 6];
+    for (int i = 0; i < 8 * nb; ++i) sc[i] = C2<T>::zero;
+    const T* cc = coeffs + c * 4 * nb;
+    for (int qp = 0; qp < nqv; ++qp) {
+        const T w = vol_w[c * nqv + qp];
+        if (w == C2<T>::zero) continue;
+        T qv[4];
+        trace4(vol_basis + (c * nqv + qp) * nb, cc, nb, qv);
+        for (int j = 0; j < nb; ++j) {
+            const T gx = w * vol_gx[(c * nqv + qp) * nb + j];
+            const T gy = w * vol_gy[(c * nqv + qp) * nb + j];
+            for (int v = 0; v < 4; ++v) sc[v * nb + j] -= qv[v] * gx;
+            for (int v = 0; v < 4; ++v) sc[(4 + v) * nb + j] -= qv[v] * gy;
+        }
+    }
+    for (int slot = 0; slot < cell_nfaces[c]; ++slot) {
+        const int64_t fid = cell_faces[c * maxf + slot];
+        const int sgn = cell_fsign[c * maxf + slot];
+        const T* tb = sgn > 0 ? fbL : fbR;
+        const T s = T(sgn);
+        const T nx = fnx[fid], ny = fny[fid];
+        for (int q = 0; q < nqf; ++q) {
+            const T w = s * face_w[fid * nqf + q];
+            const T* h = qhat + (fid * nqf + q) * 4;
+            const T wx = w * nx;
+            const T wy = w * ny;
+            for (int j = 0; j < nb; ++j) {
+                const T b = tb[(fid * nqf + q) * nb + j];
+                for (int v = 0; v < 4; ++v) sc[v * nb + j] += h[v] * wx * b;
+                for (int v = 0; v < 4; ++v) sc[(4 + v) * nb + j] += h[v] * wy * b;
+            }
+        }
+    }
+    const T* mi = minv + c * nb * nb;
+    for (int dv = 0; dv < 8; ++dv)
+        for (int j = 0; j < nb; ++j) {
+            T acc = C2<T>::zero;
+            for (int k = 0; k < nb; ++k) acc += mi[j * nb + k] * sc[dv * nb + k];
+            aux[(c * 8 + dv) * nb + j] = acc;
+        }
+}
+
+// hodg/dg.py:240-351: thread per face; VIS = the ivis == 1 branch
+template <typename T, bool VIS>
+__global__ void flux_pass2d(int64_t n_faces, int nqf, int nb, const T* __restrict__ coeffs, const T* __restrict__ aux,
+                            const T* __restrict__ fbL, const T* __restrict__ fbR,
+                            const int32_t* __restrict__ face_cells, const int8_t* __restrict__ bc_code,
+                            const T* __restrict__ fnx, const T* __restrict__ fny, const T* __restrict__ qinf,
+                            double gamma, double Rgas, double mu, double Pr, int flux_kind, T* __restrict__ finv,
+                            T* __restrict__ fvis, T* __restrict__ fqhat, uint8_t* __restrict__ errf) {
+    const int64_t f = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (f >= n_faces) return;
+    const T g = T(gamma);
+    const T R = T(Rgas), m = T(mu), pr = T(Pr);
     const int64_t iL = face_cells[2 * f], iR = face_cells[2 * f + 1];
     const T nx = fnx[f], ny = fny[f];
     for (int q = 0; q < nqf; ++q) {
@@ -181,10 +341,23 @@ __global__ void flux_pass2d(int64_t n_faces, int nqf, int nb, const T* __restric
             const T b = fbL[(f * nqf + q) * nb + k];
             for (int v = 0; v < 4; ++v) qL[v] += b * coeffs[(iL * 4 + v) * nb + k];
         }
+        T zLx[4], zLy[4], zRx[4], zRy[4];
+        if (VIS) {
+            trace4(fbL + (f * nqf + q) * nb, aux + iL * 8 * nb, nb, zLx);
+            trace4(fbL + (f * nqf + q) * nb, aux + (iL * 8 + 4) * nb, nb, zLy);
+            for (int v = 0; v < 4; ++v) {
+                zRx[v] = zLx[v];
+                zRy[v] = zLy[v];
+            }
+        }
         if (iR >= 0) {
             for (int k = 0; k < nb; ++k) {
                 const T b = fbR[(f * nqf + q) * nb + k];
                 for (int v = 0; v < 4; ++v) qR[v] += b * coeffs[(iR * 4 + v) * nb + k];
+            }
+            if (VIS) {
+                trace4(fbR + (f * nqf + q) * nb, aux + iR * 8 * nb, nb, zRx);
+                trace4(fbR + (f * nqf + q) * nb, aux + (iR * 8 + 4) * nb, nb, zRy);
             }
         } else {
             if (qL[0] <= C2<T>::zero) {
@@ -207,22 +380,34 @@ __global__ void flux_pass2d(int64_t n_faces, int nqf, int nb, const T* __restric
             continue;
         }
         for (int v = 0; v < 4; ++v) finv[(f * nqf + q) * 4 + v] = h[v];
+        if (VIS) {
+            T hL[4], hR[4];
+            viscn2(qL, zLx, zLy, nx, ny, g, R, m, pr, hL);
+            viscn2(qR, zRx, zRy, nx, ny, g, R, m, pr, hR);
+            for (int v = 0; v < 4; ++v) {
+                fvis[(f * nqf + q) * 4 + v] = C2<T>::half * (hL[v] + hR[v]);
+                fqhat[(f * nqf + q) * 4 + v] = C2<T>::half * (qL[v] + qR[v]);
+            }
+        }
     }
 }
 
-// hodg/dg.py:353-460 (Euler branch): thread per cell; products at T,
-// accumulation and the mass solve in double
-template <typename T>
+// hodg/dg.py:353-460: thread per cell; products at T, accumulation and the
+// mass solve in double; VIS = the ivis == 1 branch
+template <typename T, bool VIS>
 __global__ void rhs_pass2d(int64_t n_cells, int nb, int nqv, int nqf, int maxf, const T* __restrict__ coeffs,
-                           const T* __restrict__ finv, const T* __restrict__ vol_w, const T* __restrict__ vol_basis,
+                           const T* __restrict__ aux, const T* __restrict__ finv, const T* __restrict__ fvis,
+                           const T* __restrict__ vol_w, const T* __restrict__ vol_basis,
                            const T* __restrict__ vol_gx, const T* __restrict__ vol_gy,
                            const int8_t* __restrict__ cell_nfaces, const int32_t* __restrict__ cell_faces,
                            const int8_t* __restrict__ cell_fsign, const T* __restrict__ face_w,
                            const T* __restrict__ fbL, const T* __restrict__ fbR, const double* __restrict__ minv64,
-                           double gamma, double* __restrict__ res, uint8_t* __restrict__ errc) {
+                           double gamma, double Rgas, double mu, double Pr, double* __restrict__ res,
+                           uint8_t* __restrict__ errc) {
     const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (c >= n_cells) return;
     const T g = T(gamma);
+    const T R = T(Rgas), m = T(mu), pr = T(Pr);
     double sc[4 * 6];  // nb <= 6 (order <= 2)
     for (int i = 0; i < 4 * nb; ++i) sc[i] = 0.0;
     const T* cc = coeffs + c * 4 * nb;
@@ -244,8 +429,21 @@ __global__ void rhs_pass2d(int64_t n_cells, int nb, int nqv, int nqf, int maxf, 
             errc[c] = 1;
             continue;
         }
-        const T ex[4] = {qv[1], qv[1] * u + p, qv[1] * vv, (qv[3] + p) * u};
-        const T fy[4] = {qv[2], qv[2] * u, qv[2] * vv + p, (qv[3] + p) * vv};
+        T ex[4] = {qv[1], qv[1] * u + p, qv[1] * vv, (qv[3] + p) * u};
+        T fy[4] = {qv[2], qv[2] * u, qv[2] * vv + p, (qv[3] + p) * vv};
+        if (VIS) {
+            T zx[4], zy[4], gr[8], st[5];
+            trace4(vol_basis + (c * nqv + qp) * nb, aux + c * 8 * nb, nb, zx);
+            trace4(vol_basis + (c * nqv + qp) * nb, aux + (c * 8 + 4) * nb, nb, zy);
+            vel_temp_grads2(qv[0], qv[1], qv[2], qv[3], zx, zy, g, R, gr);
+            stress_heat2(gr, g, R, m, pr, st);
+            ex[1] -= st[0];
+            ex[2] -= st[1];
+            ex[3] -= gr[0] * st[0] + gr[1] * st[1] - st[3];
+            fy[1] -= st[1];
+            fy[2] -= st[2];
+            fy[3] -= gr[0] * st[1] + gr[1] * st[2] - st[4];
+        }
         for (int j = 0; j < nb; ++j) {
             const T gx = w * vol_gx[(c * nqv + qp) * nb + j];
             const T gy = w * vol_gy[(c * nqv + qp) * nb + j];
@@ -259,7 +457,10 @@ __global__ void rhs_pass2d(int64_t n_cells, int nb, int nqv, int nqf, int maxf, 
         const T s = T(sgn);
         for (int q = 0; q < nqf; ++q) {
             const T w = s * face_w[fid * nqf + q];
-            const T* h = finv + (fid * nqf + q) * 4;
+            T h[4];
+            for (int v = 0; v < 4; ++v) h[v] = finv[(fid * nqf + q) * 4 + v];
+            if (VIS)
+                for (int v = 0; v < 4; ++v) h[v] -= fvis[(fid * nqf + q) * 4 + v];
             for (int j = 0; j < nb; ++j) {
                 const T wb = w * tb[(fid * nqf + q) * nb + j];
                 for (int v = 0; v < 4; ++v) sc[v * nb + j] -= h[v] * wb;
@@ -326,27 +527,66 @@ __global__ void combine2d(int64_t n, int per, const T* __restrict__ u, const T* 
 inline unsigned nblk(int64_t n) { return unsigned((n + 127) / 128); }
 inline int rc() { return cudaGetLastError() == cudaSuccess ? HODG_OK : HODG_ECUDA; }
 
-}  // namespace
+template <bool VIS>
+int flux2d_dispatch(int prec, int64_t n_faces, int nqf, int nb, const void* coeffs, const void* aux, const void* fbL,
+                    const void* fbR, const int32_t* face_cells, const int8_t* bc_code, const void* fnx,
+                    const void* fny, const void* qinf, double gamma, double Rgas, double mu, double Pr, int flux_kind,
+                    void* finv, void* fvis, void* fqhat, uint8_t* errf, void* stream) {
+    if (n_faces <= 0 || nb < 1 || nb > 6 || nqf < 1) return HODG_EINVAL;
+    hodg_count_launch(1);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+#define HODG_FLUX_ARGS(T)                                                                                            \
+    n_faces, nqf, nb, (const T*)coeffs, (const T*)aux, (const T*)fbL, (const T*)fbR, face_cells, bc_code,           \
+        (const T*)fnx, (const T*)fny, (const T*)qinf, gamma, Rgas, mu, Pr, flux_kind, (T*)finv, (T*)fvis, (T*)fqhat, \
+        errf
+    if (prec == HODG_PREC_F64)
+        flux_pass2d<double, VIS><<<nblk(n_faces), 128, 0, st>>>(HODG_FLUX_ARGS(double));
+    else
+        flux_pass2d<float, VIS><<<nblk(n_faces), 128, 0, st>>>(HODG_FLUX_ARGS(float));
+#undef HODG_FLUX_ARGS
+    return rc();
+}
 
-extern int64_t hodg_count_launch(int64_t n);
+template <bool VIS>
+int rhs2d_dispatch(int prec, int64_t n_cells, int nb, int nqv, int nqf, int maxf, const void* coeffs,
+                   const void* aux, const void* finv, const void* fvis, const void* vol_w, const void* vol_basis,
+                   const void* vol_gx, const void* vol_gy, const int8_t* cell_nfaces, const int32_t* cell_faces,
+                   const int8_t* cell_fsign, const void* face_w, const void* fbL, const void* fbR,
+                   const double* minv64, double gamma, double Rgas, double mu, double Pr, double* res, uint8_t* errc,
+                   void* stream) {
+    if (n_cells <= 0 || nb < 1 || nb > 6) return HODG_EINVAL;
+    hodg_count_launch(1);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+#define HODG_RHS_ARGS(T)                                                                                             \
+    n_cells, nb, nqv, nqf, maxf, (const T*)coeffs, (const T*)aux, (const T*)finv, (const T*)fvis, (const T*)vol_w,   \
+        (const T*)vol_basis, (const T*)vol_gx, (const T*)vol_gy, cell_nfaces, cell_faces, cell_fsign,               \
+        (const T*)face_w, (const T*)fbL, (const T*)fbR, minv64, gamma, Rgas, mu, Pr, res, errc
+    if (prec == HODG_PREC_F64)
+        rhs_pass2d<double, VIS><<<nblk(n_cells), 128, 0, st>>>(HODG_RHS_ARGS(double));
+    else
+        rhs_pass2d<float, VIS><<<nblk(n_cells), 128, 0, st>>>(HODG_RHS_ARGS(float));
+#undef HODG_RHS_ARGS
+    return rc();
+}
+
+}  // namespace
 
 extern "C" {
 
 int hodg2d_flux_pass(int prec, int64_t n_faces, int nqf, int nb, const void* coeffs, const void* fbL, const void* fbR,
                      const int32_t* face_cells, const int8_t* bc_code, const void* fnx, const void* fny,
                      const void* qinf, double gamma, int flux_kind, void* finv, uint8_t* errf, void* stream) {
-    if (n_faces <= 0 || nb < 1 || nb > 6 || nqf < 1) return HODG_EINVAL;
-    hodg_count_launch(1);
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (prec == HODG_PREC_F64)
-        flux_pass2d<double><<<nblk(n_faces), 128, 0, st>>>(
-            n_faces, nqf, nb, (const double*)coeffs, (const double*)fbL, (const double*)fbR, face_cells, bc_code,
-            (const double*)fnx, (const double*)fny, (const double*)qinf, gamma, flux_kind, (double*)finv, errf);
-    else
-        flux_pass2d<float><<<nblk(n_faces), 128, 0, st>>>(
-            n_faces, nqf, nb, (const float*)coeffs, (const float*)fbL, (const float*)fbR, face_cells, bc_code,
-            (const float*)fnx, (const float*)fny, (const float*)qinf, gamma, flux_kind, (float*)finv, errf);
-    return rc();
+    return flux2d_dispatch<false>(prec, n_faces, nqf, nb, coeffs, nullptr, fbL, fbR, face_cells, bc_code, fnx, fny,
+                                  qinf, gamma, 1.0, 0.0, 1.0, flux_kind, finv, nullptr, nullptr, errf, stream);
+}
+
+int hodg2d_flux_pass_ns(int prec, int64_t n_faces, int nqf, int nb, const void* coeffs, const void* aux,
+                        const void* fbL, const void* fbR, const int32_t* face_cells, const int8_t* bc_code,
+                        const void* fnx, const void* fny, const void* qinf, double gamma, double Rgas, double mu,
+                        double Pr, void* finv, void* fvis, void* fqhat, uint8_t* errf, void* stream) {
+    if (aux == nullptr || fvis == nullptr || fqhat == nullptr) return HODG_EINVAL;
+    return flux2d_dispatch<true>(prec, n_faces, nqf, nb, coeffs, aux, fbL, fbR, face_cells, bc_code, fnx, fny, qinf,
+                                 gamma, Rgas, mu, Pr, HODG_FLUX_ROE, finv, fvis, fqhat, errf, stream);
 }
 
 int hodg2d_rhs_pass(int prec, int64_t n_cells, int nb, int nqv, int nqf, int maxf, const void* coeffs,
@@ -354,19 +594,57 @@ int hodg2d_rhs_pass(int prec, int64_t n_cells, int nb, int nqv, int nqf, int max
                     const void* vol_gy, const int8_t* cell_nfaces, const int32_t* cell_faces,
                     const int8_t* cell_fsign, const void* face_w, const void* fbL, const void* fbR,
                     const double* minv64, double gamma, double* res, uint8_t* errc, void* stream) {
-    if (n_cells <= 0 || nb < 1 || nb > 6) return HODG_EINVAL;
+    return rhs2d_dispatch<false>(prec, n_cells, nb, nqv, nqf, maxf, coeffs, nullptr, finv, nullptr, vol_w, vol_basis,
+                                 vol_gx, vol_gy, cell_nfaces, cell_faces, cell_fsign, face_w, fbL, fbR, minv64, gamma,
+                                 1.0, 0.0, 1.0, res, errc, stream);
+}
+
+int hodg2d_rhs_pass_ns(int prec, int64_t n_cells, int nb, int nqv, int nqf, int maxf, const void* coeffs,
+                       const void* aux, const void* finv, const void* fvis, const void* vol_w, const void* vol_basis,
+                       const void* vol_gx, const void* vol_gy, const int8_t* cell_nfaces, const int32_t* cell_faces,
+                       const int8_t* cell_fsign, const void* face_w, const void* fbL, const void* fbR,
+                       const double* minv64, double gamma, double Rgas, double mu, double Pr, double* res,
+                       uint8_t* errc, void* stream) {
+    if (aux == nullptr || fvis == nullptr) return HODG_EINVAL;
+    return rhs2d_dispatch<true>(prec, n_cells, nb, nqv, nqf, maxf, coeffs, aux, finv, fvis, vol_w, vol_basis, vol_gx,
+                                vol_gy, cell_nfaces, cell_faces, cell_fsign, face_w, fbL, fbR, minv64, gamma, Rgas,
+                                mu, Pr, res, errc, stream);
+}
+
+int hodg2d_qhat_pass(int prec, int64_t n_faces, int nqf, int nb, const void* coeffs, const void* fbL, const void* fbR,
+                     const int32_t* face_cells, const int8_t* bc_code, const void* fnx, const void* fny,
+                     const void* qinf, double gamma, void* qhat, uint8_t* errf, void* stream) {
+    if (n_faces <= 0 || nb < 1 || nb > 6 || nqf < 1) return HODG_EINVAL;
     hodg_count_launch(1);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (prec == HODG_PREC_F64)
-        rhs_pass2d<double><<<nblk(n_cells), 128, 0, st>>>(
-            n_cells, nb, nqv, nqf, maxf, (const double*)coeffs, (const double*)finv, (const double*)vol_w,
-            (const double*)vol_basis, (const double*)vol_gx, (const double*)vol_gy, cell_nfaces, cell_faces,
-            cell_fsign, (const double*)face_w, (const double*)fbL, (const double*)fbR, minv64, gamma, res, errc);
+        qhat_pass2d<double><<<nblk(n_faces), 128, 0, st>>>(
+            n_faces, nqf, nb, (const double*)coeffs, (const double*)fbL, (const double*)fbR, face_cells, bc_code,
+            (const double*)fnx, (const double*)fny, (const double*)qinf, gamma, (double*)qhat, errf);
     else
-        rhs_pass2d<float><<<nblk(n_cells), 128, 0, st>>>(
-            n_cells, nb, nqv, nqf, maxf, (const float*)coeffs, (const float*)finv, (const float*)vol_w,
-            (const float*)vol_basis, (const float*)vol_gx, (const float*)vol_gy, cell_nfaces, cell_faces,
-            cell_fsign, (const float*)face_w, (const float*)fbL, (const float*)fbR, minv64, gamma, res, errc);
+        qhat_pass2d<float><<<nblk(n_faces), 128, 0, st>>>(
+            n_faces, nqf, nb, (const float*)coeffs, (const float*)fbL, (const float*)fbR, face_cells, bc_code,
+            (const float*)fnx, (const float*)fny, (const float*)qinf, gamma, (float*)qhat, errf);
+    return rc();
+}
+
+int hodg2d_aux_pass(int prec, int64_t n_cells, int nb, int nqv, int nqf, int maxf, const void* coeffs,
+                    const void* qhat, const void* vol_w, const void* vol_basis, const void* vol_gx,
+                    const void* vol_gy, const int8_t* cell_nfaces, const int32_t* cell_faces,
+                    const int8_t* cell_fsign, const void* face_w, const void* fbL, const void* fbR, const void* fnx,
+                    const void* fny, const void* minv, void* aux, void* stream) {
+    if (n_cells <= 0 || nb < 1 || nb > 6) return HODG_EINVAL;
+    hodg_count_launch(1);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+#define HODG_AUX_ARGS(T)                                                                                             \
+    n_cells, nb, nqv, nqf, maxf, (const T*)coeffs, (const T*)qhat, (const T*)vol_w, (const T*)vol_basis,             \
+        (const T*)vol_gx, (const T*)vol_gy, cell_nfaces, cell_faces, cell_fsign, (const T*)face_w, (const T*)fbL,    \
+        (const T*)fbR, (const T*)fnx, (const T*)fny, (const T*)minv, (T*)aux
+    if (prec == HODG_PREC_F64)
+        aux_pass2d<double><<<nblk(n_cells), 128, 0, st>>>(HODG_AUX_ARGS(double));
+    else
+        aux_pass2d<float><<<nblk(n_cells), 128, 0, st>>>(HODG_AUX_ARGS(float));
+#undef HODG_AUX_ARGS
     return rc();
 }
 

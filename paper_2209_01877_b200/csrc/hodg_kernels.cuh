@@ -162,8 +162,6 @@ __global__ void __launch_bounds__(FACE_THREADS, 4) face_flux_kernel(const hodg_m
     const int rem = t - side * FT * NG;
     const int lf = rem / NG;
     const int g = rem - lf * NG;
-    const int64_t ntiles = (f_end - f_begin + FT - 1) / FT;
-
     if (t == 0) {
         mbar_init(bar, FACE_THREADS);
         mbar_init(bar + 1, FACE_THREADS);
@@ -177,32 +175,36 @@ __global__ void __launch_bounds__(FACE_THREADS, 4) face_flux_kernel(const hodg_m
         fbt[s * FBS + (k - s * NQF * NB)] = fbg[k];
     }
 
-    // per-tile metadata of this thread's (face, side): element, slot, and
-    // (side 0, group 0 threads) the face's bc / right flag / normal
+    // per-tile metadata of this thread's (face, side): raw element id and
+    // face info word (decoded only when consumed, so the loads issued for
+    // the next tile stay in flight across this tile's work), and for the
+    // (side 0, group 0) threads the right-element id and the normal
     struct Meta {
-        int64_t elem;
-        int slot;
-        int finf;
+        int elem;
+        int info;
+        int right;
         double4 nrm;
     };
-    auto load_meta = [&](int64_t tile) {
-        Meta mt{-1, 0, 0, make_double4(0, 0, 0, 0)};
-        const int64_t f0 = f_begin + tile * FT;
+    const int ntiles = int((f_end - f_begin + FT - 1) / FT);
+    auto load_meta = [&](int tile) {
+        Meta mt{-1, 0, -1, make_double4(0, 0, 0, 0)};
+        const int64_t f0 = f_begin + int64_t(tile) * FT;
         if (tile < ntiles && f0 + lf < f_end) {
             const int64_t f = f0 + lf;
-            mt.elem = m.fcells[2 * f + side];
-            const int info = m.finfo[f];
-            mt.slot = side == 0 ? (info & 3) : ((info >> 2) & 3);
+            mt.elem = __ldg(m.fcells + 2 * f + side);
+            mt.info = __ldg(m.finfo + f);
             if (side == 0 && g == 0) {
-                mt.finf = ((info >> 4) & 15) | (m.fcells[2 * f + 1] >= 0 ? 0x100 : 0);
-                mt.nrm = reinterpret_cast<const double4*>(m.fnrm)[f];
+                mt.right = __ldg(m.fcells + 2 * f + 1);
+                const double2 a = __ldg(reinterpret_cast<const double2*>(m.fnrm) + 2 * f);
+                const double2 b = __ldg(reinterpret_cast<const double2*>(m.fnrm) + 2 * f + 1);
+                mt.nrm = make_double4(a.x, a.y, b.x, b.y);
             }
         }
         return mt;
     };
     auto publish = [&](const Meta& mt, int buf) {
         if (side == 0 && g == 0) {
-            finf[buf][lf] = mt.finf;
+            finf[buf][lf] = ((mt.info >> 4) & 15) | (mt.right >= 0 ? 0x100 : 0);
             fn[buf][lf][0] = mt.nrm.x;
             fn[buf][lf][1] = mt.nrm.y;
             fn[buf][lf][2] = mt.nrm.z;
@@ -210,20 +212,20 @@ __global__ void __launch_bounds__(FACE_THREADS, 4) face_flux_kernel(const hodg_m
         double* row = rows0 + buf * BUF + size_t(side * FT + lf) * RS;
         if (g == 0 && mt.elem >= 0) {
             mbar_arrive_expect_tx(bar + buf, RS * 8);
-            bulk_g2s(row, state + mt.elem * RS, RS * 8, bar + buf);
+            bulk_g2s(row, state + int64_t(mt.elem) * RS, RS * 8, bar + buf);
         } else {
             mbar_arrive(bar + buf);
         }
     };
 
-    int64_t tile = blockIdx.x;
+    int tile = blockIdx.x;
     Meta cur = load_meta(tile);
     __syncthreads();  // barrier init visible
     if (tile < ntiles) publish(cur, 0);
     const T gam = T(m.gamma);
     for (int it = 0; tile < ntiles; tile += gridDim.x, ++it) {
         const int buf = it & 1;
-        const int64_t f0 = f_begin + tile * FT;
+        const int64_t f0 = f_begin + int64_t(tile) * FT;
         const int nf = int(min(int64_t(FT), f_end - f0));
         const Meta nxt = load_meta(tile + gridDim.x);  // in flight during this tile
         mbar_wait(bar + buf, (it >> 1) & 1);
@@ -236,7 +238,8 @@ __global__ void __launch_bounds__(FACE_THREADS, 4) face_flux_kernel(const hodg_m
 #pragma unroll
             for (int v = 0; v < 5; ++v) tr[qq][v] = T(0);
         if (cur.elem >= 0) {
-            const T* fb = fbt + cur.slot * FBS;
+            const int slot = side == 0 ? (cur.info & 3) : ((cur.info >> 2) & 3);
+            const T* fb = fbt + slot * FBS;
 #pragma unroll
             for (int i = 0; i < NB; ++i) {
                 T c[5];

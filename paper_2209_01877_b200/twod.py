@@ -318,6 +318,21 @@ def vortex_2d(gamma, R, mach, angle_deg, beta, x0, y0, x, y):
     return rho, u, v, rho * R * T
 
 
+def pulse_2d(gamma, R, amplitude, sigma, x0, y0, x, y, mach=0.0, angle_deg=0.0):
+    """hodg/flows.py:60-73."""
+    x = np.asarray(x, dtype=np.float64)
+    y = np.asarray(y, dtype=np.float64)
+    r2 = (x - x0) ** 2 + (y - y0) ** 2
+    p = R * (1.0 + amplitude * np.exp(-0.5 * r2 / (sigma * sigma)))
+    rho = (p / R) ** (1.0 / gamma)
+    if mach > 0.0:
+        (_, ui, vi, _), _ = freestream_2d(gamma, R, mach, angle_deg)
+        u, v = np.full_like(p, ui), np.full_like(p, vi)
+    else:
+        u, v = np.zeros_like(p), np.zeros_like(p)
+    return rho, u, v, p
+
+
 def project_2d(m: Mesh2D, t: Tables2D, prim, gamma):
     x = t.vol_xy[:, :, 0].ravel()
     rho, u, v, p = (np.broadcast_to(np.asarray(a, dtype=np.float64), x.shape) for a in prim)
@@ -336,11 +351,17 @@ def project_2d(m: Mesh2D, t: Tables2D, prim, gamma):
 class Device2D:
     """Tables uploaded once per precision; passes over device arrays."""
 
-    def __init__(self, m: Mesh2D, t: Tables2D, gamma, qinf, flux_kind=0, mu=0.0, device="cuda"):
+    def __init__(self, m: Mesh2D, t: Tables2D, gamma, qinf, flux_kind=0, mu=0.0, device="cuda", R=1.0, Pr=0.72,
+                 ivis=0):
         import torch
 
         self.L = _lib.lib()
         self.m, self.t, self.gamma, self.mu, self.flux_kind = m, t, float(gamma), float(mu), flux_kind
+        self.R, self.Pr, self.ivis = float(R), float(Pr), int(ivis)
+        if self.ivis not in (0, 1):
+            raise ValueError("ivis must be 0 or 1")
+        if self.ivis and flux_kind != 0:
+            raise ValueError("the viscous passes use the Roe flux, as the reference's")
         self.dev = torch.device(device)
         self.qinf = np.asarray(qinf, dtype=np.float64)
         bc = m.boundary_kind_codes()
@@ -372,7 +393,8 @@ class Device2D:
             t, m = self.t, self.m
             d = dict(fbL=up(t.fbl, dt), fbR=up(t.fbr, dt), fnx=up(m.face_normal[:, 0], dt),
                      fny=up(m.face_normal[:, 1], dt), qinf=up(self.qinf, dt), vol_w=up(t.vol_w, dt),
-                     vol_b=up(t.vol_basis, dt), vol_gx=up(t.vol_gx, dt), vol_gy=up(t.vol_gy, dt), face_w=up(t.face_w, dt))
+                     vol_b=up(t.vol_basis, dt), vol_gx=up(t.vol_gx, dt), vol_gy=up(t.vol_gy, dt), face_w=up(t.face_w, dt),
+                     minv=up(t.minv, dt))
             self._tabs[prec] = d
         return d
 
@@ -381,11 +403,82 @@ class Device2D:
             idx = int(err.nonzero()[0, 0])
             raise AdmissibilityError(msg, iteration=iteration, **{key: idx})
 
-    def rhs(self, coeffs, iteration=None):
-        """flux_pass then rhs_pass (hodg/dg.py:652-663); float64 residual."""
+    def _prec(self, coeffs):
         import torch
 
-        prec = _lib.PREC_F64 if coeffs.dtype == torch.float64 else _lib.PREC_MIXED
+        return _lib.PREC_F64 if coeffs.dtype == torch.float64 else _lib.PREC_MIXED
+
+    def aux_gradient(self, coeffs, iteration=None):
+        """compute_aux_gradient (hodg/dg.py:572-591): qhat_pass + aux_pass;
+        returns z as (n_cells, 2, 4, nb) at the state precision."""
+        import torch
+
+        prec = self._prec(coeffs)
+        d = self.tabs(prec)
+        m, t = self.m, self.t
+        nqf = t.face_w.shape[1]
+        P, s = _lib.ptr, _lib.stream_ptr()
+        qhat = torch.zeros((m.n_faces, nqf, 4), dtype=coeffs.dtype, device=self.dev)
+        self.errf.zero_()
+        _lib.check(self.L.hodg2d_qhat_pass(prec, m.n_faces, nqf, t.nb, P(coeffs), P(d["fbL"]), P(d["fbR"]),
+                                           P(self.face_cells), P(self.bc), P(d["fnx"]), P(d["fny"]), P(d["qinf"]),
+                                           self.gamma, P(qhat), P(self.errf), s), "hodg2d_qhat_pass")
+        self._raise(self.errf, "inadmissible face trace", "face", iteration)
+        aux = torch.empty((m.n_cells, 2, 4, t.nb), dtype=coeffs.dtype, device=self.dev)
+        _lib.check(self.L.hodg2d_aux_pass(prec, m.n_cells, t.nb, t.vol_w.shape[1], nqf, 4, P(coeffs), P(qhat),
+                                          P(d["vol_w"]), P(d["vol_b"]), P(d["vol_gx"]), P(d["vol_gy"]),
+                                          P(self.cell_nv), P(self.cell_faces), P(self.cell_fsign), P(d["face_w"]),
+                                          P(d["fbL"]), P(d["fbR"]), P(d["fnx"]), P(d["fny"]), P(d["minv"]), P(aux),
+                                          s), "hodg2d_aux_pass")
+        return aux
+
+    def face_flux_ns(self, coeffs, aux, iteration=None):
+        """face_flux_pass with ivis = 1 (hodg/dg.py:594-621): (finv, fvis, fqhat)."""
+        import torch
+
+        prec = self._prec(coeffs)
+        d = self.tabs(prec)
+        m, t = self.m, self.t
+        nqf = t.face_w.shape[1]
+        P, s = _lib.ptr, _lib.stream_ptr()
+        finv, fvis, fqhat = (torch.zeros((m.n_faces, nqf, 4), dtype=coeffs.dtype, device=self.dev) for _ in range(3))
+        self.errf.zero_()
+        _lib.check(self.L.hodg2d_flux_pass_ns(prec, m.n_faces, nqf, t.nb, P(coeffs), P(aux), P(d["fbL"]),
+                                              P(d["fbR"]), P(self.face_cells), P(self.bc), P(d["fnx"]), P(d["fny"]),
+                                              P(d["qinf"]), self.gamma, self.R, self.mu, self.Pr, P(finv), P(fvis),
+                                              P(fqhat), P(self.errf), s), "hodg2d_flux_pass_ns")
+        self._raise(self.errf, "inadmissible face trace", "face", iteration)
+        return finv, fvis, fqhat
+
+    def accumulate_ns(self, coeffs, aux, finv, fvis, iteration=None):
+        """accumulate_rhs with ivis = 1 (hodg/dg.py:624-649); float64 residual."""
+        import torch
+
+        prec = self._prec(coeffs)
+        d = self.tabs(prec)
+        m, t = self.m, self.t
+        P, s = _lib.ptr, _lib.stream_ptr()
+        res = torch.empty((m.n_cells, 4, t.nb), dtype=torch.float64, device=self.dev)
+        self.errc.zero_()
+        _lib.check(self.L.hodg2d_rhs_pass_ns(prec, m.n_cells, t.nb, t.vol_w.shape[1], t.face_w.shape[1], 4,
+                                             P(coeffs), P(aux), P(finv), P(fvis), P(d["vol_w"]), P(d["vol_b"]),
+                                             P(d["vol_gx"]), P(d["vol_gy"]), P(self.cell_nv), P(self.cell_faces),
+                                             P(self.cell_fsign), P(d["face_w"]), P(d["fbL"]), P(d["fbR"]),
+                                             P(self.minv), self.gamma, self.R, self.mu, self.Pr, P(res), P(self.errc),
+                                             s), "hodg2d_rhs_pass_ns")
+        self._raise(self.errc, "inadmissible volume state", "cell", iteration)
+        return res
+
+    def rhs(self, coeffs, iteration=None):
+        """aux gradient (viscous runs only), flux_pass, rhs_pass
+        (hodg/dg.py:652-663); float64 residual."""
+        import torch
+
+        if self.ivis:
+            aux = self.aux_gradient(coeffs, iteration)
+            finv, fvis, _ = self.face_flux_ns(coeffs, aux, iteration)
+            return self.accumulate_ns(coeffs, aux, finv, fvis, iteration)
+        prec = self._prec(coeffs)
         d = self.tabs(prec)
         m, t = self.m, self.t
         nqf = t.face_w.shape[1]
@@ -447,22 +540,40 @@ class RunConfig2D:
     gen_bc: object = "far_field"
     gamma: float = 1.4
     R: float = 1.0
+    mu_dyn: float | None = None
+    Pr: float = 0.72
+    ivis: int = 0
     mach: float = 0.3
     angle_deg: float = 0.0
-    initial_kind: str = "freestream"
+    reynolds: float | None = None
+    initial_kind: str = "freestream"  # freestream | vortex | pulse
     vortex_beta: float = 5.0
     initial_x0: float = 0.0
     initial_y0: float = 0.0
+    pulse_amplitude: float = 0.2
+    pulse_sigma: float = 0.1
     order: int = 1
     cfl: float = 0.3
     dt_mode: str = "local"
+    dt_floor: float = 0.0
+    dt_fixed: float | None = None
+    t_final: float | None = None
     max_iterations: int = 100
+    residual_target: float | None = None
     log_every: int = 1
     precision_mode: str = "dp"
     switch_iter: int = 0
     window: int = 200
     factor: float = 2.0
     flux_kind: int = 0
+
+    def mu(self) -> float:
+        """hodg/config.py:102-111: explicit mu, else Mach * a / Re for viscous runs."""
+        if self.mu_dyn is not None:
+            return float(self.mu_dyn)
+        if self.ivis and self.reynolds:
+            return self.mach * (self.gamma * self.R) ** 0.5 / self.reynolds
+        return 0.0
 
 
 @dataclass
@@ -486,31 +597,53 @@ def run2d(cfg: RunConfig2D):
     if cfg.initial_kind == "vortex":
         prim = vortex_2d(cfg.gamma, cfg.R, cfg.mach, cfg.angle_deg, cfg.vortex_beta, cfg.initial_x0,
                          cfg.initial_y0, x, y)
+    elif cfg.initial_kind == "pulse":
+        prim = pulse_2d(cfg.gamma, cfg.R, cfg.pulse_amplitude, cfg.pulse_sigma, cfg.initial_x0, cfg.initial_y0, x, y,
+                        cfg.mach, cfg.angle_deg)
     else:
         prim = prim_inf
     u = torch.from_numpy(project_2d(m, t, prim, cfg.gamma)).cuda()
-    dev = Device2D(m, t, cfg.gamma, qinf, cfg.flux_kind)
+    dev = Device2D(m, t, cfg.gamma, qinf, cfg.flux_kind, mu=cfg.mu(), R=cfg.R, Pr=cfg.Pr, ivis=cfg.ivis)
     ctrl = PrecisionController(PrecisionSchedule(cfg.precision_mode, cfg.switch_iter, cfg.window, cfg.factor))
     sched = ctrl.schedule
     if sched.mode in ("sp", "mp_rebound") or (sched.mode == "mp_fixed" and sched.switch_iter > 0):
         u = u.to(torch.float32)
     hist = History2D()
     area = m.cell_area
+    t_sim = 0.0
     for it in range(cfg.max_iterations):
         bits, _ = ctrl.decide(it, [r[0] for r in hist.res])
         if bits == 64 and u.dtype == torch.float32:
             u = u.to(torch.float64)
         dts = dev.local_dt(u, cfg.cfl, cfg.order, it)
-        dmin = float(dts.min().item())
-        dtv = torch.full_like(dts, dmin) if cfg.dt_mode == "global" else dts
+        if cfg.dt_floor > 0.0:
+            dts = torch.clamp_min(dts, cfg.dt_floor)
+        if cfg.dt_mode == "global":
+            dmin = cfg.dt_fixed if cfg.dt_fixed is not None else float(dts.min().item())
+            if cfg.t_final is not None:
+                if t_sim >= cfg.t_final - 1e-14:
+                    break
+                dmin = min(dmin, cfg.t_final - t_sim)
+            dtv = torch.full_like(dts, dmin)
+        else:
+            dmin = float(dts.min().item())
+            dtv = dts
         u, r0 = dev.rk2_step(u, dtv, it)
+        if cfg.dt_mode == "global":
+            t_sim += dmin
         if cfg.log_every and (it % cfg.log_every == 0 or it == cfg.max_iterations - 1):
             r = r0[:, :, 0].cpu().numpy()
             res4 = np.sqrt(np.sum(area[:, None] * r * r, axis=0))  # hodg/timestepping.py:208-211
+            if not np.all(np.isfinite(res4)):
+                from .timestepping import SolverDivergedError
+
+                raise SolverDivergedError(it, hist)
             hist.iterations.append(it)
             hist.res.append(tuple(float(v) for v in res4))
             hist.dts.append(dmin)
             hist.precision.append(bits)
+            if cfg.residual_target is not None and np.all(res4 < cfg.residual_target):
+                break
     return u, hist, m, t
 
 

@@ -2,6 +2,7 @@
 oracle's (which is pinned to the reference): meshes and geometry tables."""
 
 import numpy as np
+import pytest
 
 from oracle import geometry as OG
 from oracle import mesh as OM
@@ -25,3 +26,19 @@ def test_mesh_and_tables_bitwise():
             assert np.array_equal(ta.vol_gx, tb.vol_grad[0]) and np.array_equal(ta.vol_gy, tb.vol_grad[1])
             assert np.array_equal(ta.minv, tb.minv)
             assert np.array_equal(ta.fbl, tb.face_basis_l) and np.array_equal(ta.fbr, tb.face_basis_r)
+
+
+def test_mu_from_reynolds_and_pulse_field():
+    """hodg/config.py:102-111 and hodg/flows.py:60-73 (pkg/tests/test_config.py:56-66)."""
+    from paper_2209_01877_b200 import twod
+
+    cfg = twod.RunConfig2D(gen_nx=2, gen_ny=2, ivis=1, mach=0.3, reynolds=5000.0)
+    assert cfg.mu() == pytest.approx(0.3 * 1.4 ** 0.5 / 5000.0)
+    assert twod.RunConfig2D(ivis=1, mach=0.3, reynolds=5000.0, mu_dyn=0.01).mu() == 0.01
+    assert twod.RunConfig2D(ivis=0, reynolds=5000.0).mu() == 0.0
+    x = np.linspace(-1, 1, 7)
+    rho, u, v, p = twod.pulse_2d(1.4, 1.0, 0.2, 0.3, 0.0, 0.0, x, 0 * x, 0.4, 10.0)
+    from oracle import solver as S
+    ref = S.pulse_primitive(S.Gas(), 0.2, 0.3, 0.0, 0.0, x, 0 * x, 0.4, 10.0)
+    for a, b in zip((rho, u, v, p), ref):
+        assert np.array_equal(a, b)

@@ -16,6 +16,13 @@ reference package `hodg` (numba) and writes:
                                        random states (pkg/tests/test_physics.py)
   ref_rcm.npz                          rcm permutations of seeded random graphs,
                                        including disconnected ones
+  ref_ns2d.npz                         the viscous (ivis = 1, BR1) passes on the
+                                       corpus: aux gradient, qhat, finv, fvis,
+                                       fqhat and the residual, orders 0-2, at
+                                       float64 and float32
+  residuals_ns_dp.csv,                 reference Navier-Stokes runs: a viscous
+  residuals_ns_mp.csv                  vortex (order 2) and a small version of
+                                       the c07 pulse case (mp_fixed switch)
 
 Usage:  python tools/make_golden.py
 """
@@ -107,6 +114,39 @@ def main():
             st32 = dg.DofState(st.coeffs.astype(np.float32))
             arrays[f"{name}_p{order}_res32"] = dg.rhs(st32, m, geo, bcs, gas).res
     np.savez_compressed(os.path.join(OUT, "ref_rhs2d.npz"), **arrays)
+
+    # viscous passes (pkg/tests/test_dg.py:12, mu = 0.02)
+    ns = GasModel(mu_dyn=0.02, ivis=1)
+    arrays = {}
+    for name, m in corpus():
+        for order in (0, 1, 2):
+            geo = compute_geometry(m, order)
+            bcs = dg.BoundaryConditions(flows.freestream_conserved(ns, 0.4, 10.0))
+            st = dg.project_initial(m, geo, lambda x, y: flows.vortex_primitive(
+                ns, 0.4, 10.0, 2.0, 0.5, 0.4, 0.0, x, y), ns)
+            rng = np.random.default_rng(order + 23)
+            st.coeffs[:, :, 0] *= 1.0 + 0.01 * rng.random(st.coeffs.shape[:2])
+            arrays[f"{name}_p{order}_coeffs"] = st.coeffs
+            for tag, s_ in (("", st), ("32", dg.DofState(st.coeffs.astype(np.float32)))):
+                aux = dg.compute_aux_gradient(s_, m, geo, bcs, ns)
+                buf = dg.face_flux_pass(s_, aux, m, geo, bcs, ns)
+                arrays[f"{name}_p{order}_aux{tag}"] = aux.z
+                arrays[f"{name}_p{order}_finv{tag}"] = buf.inviscid
+                arrays[f"{name}_p{order}_fvis{tag}"] = buf.viscous
+                arrays[f"{name}_p{order}_fqhat{tag}"] = buf.qhat
+                arrays[f"{name}_p{order}_res{tag}"] = dg.accumulate_rhs(s_, aux, buf, m, geo, bcs, ns).res
+    np.savez_compressed(os.path.join(OUT, "ref_ns2d.npz"), **arrays)
+    for name, kw in [
+        ("residuals_ns_dp.csv", dict(gen_kind="quad", gen_nx=12, gen_ny=12, gen_extent=(0.0, 0.0, 10.0, 10.0),
+                                     initial_kind="vortex", initial_x0=5.0, initial_y0=5.0, mach=0.5, order=2,
+                                     ivis=1, mu_dyn=0.01, max_iterations=60)),
+        ("residuals_ns_mp.csv", dict(gen_kind="quad", gen_nx=96, gen_ny=4, gen_extent=(0.0, 0.0, 12.0, 0.5),
+                                     initial_kind="pulse", initial_x0=6.0, initial_y0=0.25, pulse_amplitude=0.2,
+                                     pulse_sigma=0.3, mach=0.4, order=1, cfl=0.5, ivis=1, mu_dyn=0.002,
+                                     max_iterations=120, precision_mode="mp_fixed", switch_iter=70)),
+    ]:
+        cfg = RunConfig(log_every=1, **kw)
+        write_residual_csv(os.path.join(OUT, name), run(cfg).history)
 
     # point fluxes: Roe and boundary states on random admissible states
     rng = np.random.default_rng(2024)
