@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--order", type=int, default=2)
     ap.add_argument("--prec", type=int, default=64, choices=[64, 32])
     ap.add_argument("--no-renumber", action="store_true")
+    ap.add_argument("--layout", default="auto", choices=["auto", "elem", "face"], help="face flux record layout")
     ap.add_argument("--partitioned", action="store_true",
                     help="use the partitioned (NCCL halo) stepper even at one rank")
     return ap.parse_args()
@@ -156,7 +157,7 @@ def run_ours(args):
         state_in = owned_state(state, part)
     else:
         disc = _get_disc(mesh, geo, gas, bcs)
-        st = Stepper(disc, "rk3", prec, "global", 0.3, log_norms=True, use_graph=True)
+        st = Stepper(disc, "rk3", prec, "global", 0.3, log_norms=True, use_graph=True, layout=args.layout)
         state_in = state
     st.load(state_in)
     st.check(0)
@@ -197,7 +198,7 @@ def run_ours(args):
     value = dofs * n_st * args.steps / (ms * 1e-3)  # whole job: the global mesh
 
     # ---- per-kernel durations (events around each launch, no graph) ----
-    hb = disc.face_buffer(prec)
+    hb = st.hbuf
     t_face, t_elem = [], []
     for k in range(3 * n_st):
         stage = k % n_st
@@ -256,6 +257,13 @@ def run_ours(args):
             traffic = tr
         except Exception:
             traffic = None
+    # the FP64 roof: the stage is FP64-pipe bound; algorithmic
+    # FP64-pipe operations per stage (perf.count_flops_and_bytes, FMA = 1)
+    from paper_2209_01877_b200 import perf as PF
+
+    ops_step, _ = PF.count_flops_and_bytes(mesh, args.order, "rk3", args.prec)
+    ops_stage = ops_step / n_st
+    fp64_ops = PF.FP64_PIPE_OPS_PER_S
     line = {
         "metric": "DOF-updates/sec per RK stage (P2, 1M tets)",
         "value": value,
@@ -281,7 +289,14 @@ def run_ours(args):
                      "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
                      "kernel": "RK stage = face_flux_kernel + elem_stage_kernel",
                      "algorithmic_bytes_per_stage": alg, "stage_ms": tf + te, "face_ms": tf, "elem_ms": te,
-                     "peak_source": peak_kind},
+                     "peak_source": peak_kind,
+                     "fp64": {"achieved": ops_stage / ((tf + te) * 1e-3) / 1e12, "peak": fp64_ops / 1e12,
+                              "unit": "T FP64-pipe ops/s (FMA = 1 op)",
+                              "frac": ops_stage / ((tf + te) * 1e-3) / fp64_ops,
+                              "ops_per_stage": ops_stage,
+                              "peak_source": "profiles/fp64_peaks.md (measured DFMA 36.3 TFLOP/s)",
+                              "note": "FP64 applies to --prec 64; in mixed precision the traces and fluxes "
+                                      "run on the FP32 pipe"}},
         "clocks": clk,
         "gpu_launches": kernels_per_step * args.steps,
         "e2e": {"value": e2e, "unit": "DOF-updates/s", "h2d_bytes_per_step": state_bytes / args.steps,

@@ -133,6 +133,22 @@ int hodg_face_flux_range(const hodg_mesh* mesh, int prec, const double* state, v
                          int64_t f_end, int interior_only, uint32_t* err, void* stream);
 int hodg_elem_stage(const hodg_mesh* mesh, int prec, const void* face_buf, const hodg_stage_args* args,
                     uint32_t* err, void* stream);
+
+/* Element-slot record layout (the stepper's fused path; same values as
+ * face_buf, different placement): block e holds the records of element e's
+ * four faces, slot-major, 5 x NQF values each ([slot][var][qp]), at stride
+ * hodg_elem_record_stride(order) = 20 NQF + 1 values (odd: conflict-free
+ * per-element smem reads; a tile of hodg_elem_tile(order) blocks is one 16-byte
+ * multiple, fetched with one TMA bulk copy).  The face kernel stores each
+ * face's record into the blocks of both neighbours (owned elements only:
+ * id < n_elems), so the element kernel needs no per-face gather.  Buffer:
+ * hodg_elem_record_len(mesh, prec) values at the kernel precision. */
+int hodg_elem_record_stride(int order);
+int64_t hodg_elem_record_len(const hodg_mesh* mesh, int prec);
+int hodg_face_flux_range_es(const hodg_mesh* mesh, int prec, const double* state, void* elem_buf, int64_t f_begin,
+                            int64_t f_end, int interior_only, uint32_t* err, void* stream);
+int hodg_elem_stage_es(const hodg_mesh* mesh, int prec, const void* elem_buf, const hodg_stage_args* args,
+                       uint32_t* err, void* stream);
 int hodg_local_dt(const hodg_mesh* mesh, const double* state, double cfl, double* dt_vec_out,
                   unsigned long long* dt_min, uint32_t* err, void* stream);
 int hodg_norm_finalize(const double* partial, int64_t n_blocks, double* out5, void* stream);

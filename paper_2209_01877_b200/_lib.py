@@ -77,6 +77,10 @@ SIGNATURES = {
     "hodg_face_flux": (I32, [P, I32, P, P, P, P]),
     "hodg_face_flux_range": (I32, [P, I32, P, P, I64, I64, I32, P, P]),
     "hodg_elem_stage": (I32, [P, I32, P, C.POINTER(StageArgs), P, P]),
+    "hodg_face_flux_range_es": (I32, [P, I32, P, P, I64, I64, I32, P, P]),
+    "hodg_elem_stage_es": (I32, [P, I32, P, C.POINTER(StageArgs), P, P]),
+    "hodg_elem_record_stride": (I32, [I32]),
+    "hodg_elem_record_len": (I64, [P, I32]),
     "hodg_local_dt": (I32, [P, P, D, P, P, P, P]),
     "hodg_norm_finalize": (I32, [P, I64, P, P]),
     "hodg_residual_l2": (I32, [P, P, P, P, P]),

@@ -11,9 +11,10 @@
 
 #define DECL_ORDER(P)                                                                                          \
     int hodg_launch_face_p##P(const hodg_mesh_desc&, int, const double*, void*, uint32_t*, cudaStream_t, int64_t, \
-                              int64_t, int);                                                                   \
+                              int64_t, int, int);                                                              \
     int hodg_launch_elem_p##P(const hodg_mesh_desc&, int, const void*, const hodg_stage_args&, uint32_t*,      \
-                              cudaStream_t);                                                                   \
+                              cudaStream_t, int);                                                              \
+    int hodg_elem_record_stride_p##P();                                                                        \
     int hodg_launch_dt_p##P(const hodg_mesh_desc&, const double*, double, double*, unsigned long long*,        \
                             uint32_t*, cudaStream_t);                                                          \
     int hodg_launch_modal_p##P(const hodg_mesh_desc&, int, const double*, double*, cudaStream_t);             \
@@ -153,6 +154,15 @@ int hodg_n_basis(int order) { return (order < 0 || order > 3) ? -1 : NB_TAB[orde
 int hodg_n_face_points(int order) { return (order < 0 || order > 3) ? -1 : NQF_TAB[order]; }
 int hodg_n_vol_points(int order) { return (order < 0 || order > 3) ? -1 : NQV_TAB[order]; }
 int hodg_elem_tile(int order) { return (order < 0 || order > 3) ? -1 : TILE_TAB[order]; }
+int hodg_elem_record_stride(int order) {
+    switch (order) {
+        case 0: return hodg_elem_record_stride_p0();
+        case 1: return hodg_elem_record_stride_p1();
+        case 2: return hodg_elem_record_stride_p2();
+        case 3: return hodg_elem_record_stride_p3();
+        default: return -1;
+    }
+}
 int hodg_face_record_stride(int order, int prec) {
     if (order < 0 || order > 3 || (prec != HODG_PREC_F64 && prec != HODG_PREC_MIXED)) return -1;
     const int sz = prec == HODG_PREC_F64 ? 8 : 4;
@@ -190,20 +200,30 @@ int64_t hodg_stage_blocks(const hodg_mesh* mesh, int prec) {
     }
 }
 
-int hodg_face_flux_range(const hodg_mesh* mesh, int prec, const double* state, void* face_buf, int64_t f_begin,
-                         int64_t f_end, int interior_only, uint32_t* err, void* stream) {
-    if (!mesh || !state || !face_buf) return HODG_EINVAL;
+static int face_flux_impl(const hodg_mesh* mesh, int prec, const double* state, void* buf, int64_t f_begin,
+                          int64_t f_end, int interior_only, uint32_t* err, void* stream, int es) {
+    if (!mesh || !state || !buf) return HODG_EINVAL;
     if (prec != HODG_PREC_F64 && prec != HODG_PREC_MIXED) return HODG_EINVAL;
     if (f_begin < 0 || f_end > mesh->d.n_faces || f_begin > f_end) return HODG_EINVAL;
     if (f_begin == f_end) return HODG_OK;
     g_launches++;
     const hodg_mesh_desc& d = mesh->d;
     switch (d.order) {
-        case 0: return hodg_launch_face_p0(d, prec, state, face_buf, err, S(stream), f_begin, f_end, interior_only);
-        case 1: return hodg_launch_face_p1(d, prec, state, face_buf, err, S(stream), f_begin, f_end, interior_only);
-        case 2: return hodg_launch_face_p2(d, prec, state, face_buf, err, S(stream), f_begin, f_end, interior_only);
-        default: return hodg_launch_face_p3(d, prec, state, face_buf, err, S(stream), f_begin, f_end, interior_only);
+        case 0: return hodg_launch_face_p0(d, prec, state, buf, err, S(stream), f_begin, f_end, interior_only, es);
+        case 1: return hodg_launch_face_p1(d, prec, state, buf, err, S(stream), f_begin, f_end, interior_only, es);
+        case 2: return hodg_launch_face_p2(d, prec, state, buf, err, S(stream), f_begin, f_end, interior_only, es);
+        default: return hodg_launch_face_p3(d, prec, state, buf, err, S(stream), f_begin, f_end, interior_only, es);
     }
+}
+
+int hodg_face_flux_range(const hodg_mesh* mesh, int prec, const double* state, void* face_buf, int64_t f_begin,
+                         int64_t f_end, int interior_only, uint32_t* err, void* stream) {
+    return face_flux_impl(mesh, prec, state, face_buf, f_begin, f_end, interior_only, err, stream, 0);
+}
+
+int hodg_face_flux_range_es(const hodg_mesh* mesh, int prec, const double* state, void* elem_buf, int64_t f_begin,
+                            int64_t f_end, int interior_only, uint32_t* err, void* stream) {
+    return face_flux_impl(mesh, prec, state, elem_buf, f_begin, f_end, interior_only, err, stream, 1);
 }
 
 int hodg_face_flux(const hodg_mesh* mesh, int prec, const double* state, void* face_buf, uint32_t* err,
@@ -212,9 +232,9 @@ int hodg_face_flux(const hodg_mesh* mesh, int prec, const double* state, void* f
     return hodg_face_flux_range(mesh, prec, state, face_buf, 0, mesh->d.n_faces, 0, err, stream);
 }
 
-int hodg_elem_stage(const hodg_mesh* mesh, int prec, const void* face_buf, const hodg_stage_args* a, uint32_t* err,
-                    void* stream) {
-    if (!mesh || !face_buf || !a || !a->us) return HODG_EINVAL;
+static int elem_stage_impl(const hodg_mesh* mesh, int prec, const void* buf, const hodg_stage_args* a, uint32_t* err,
+                           void* stream, int es) {
+    if (!mesh || !buf || !a || !a->us) return HODG_EINVAL;
     if (prec != HODG_PREC_F64 && prec != HODG_PREC_MIXED) return HODG_EINVAL;
     if (a->combine < -1 || a->combine > 1) return HODG_EINVAL;
     if (a->combine >= 0 && (!a->out || !a->dt)) return HODG_EINVAL;
@@ -223,11 +243,29 @@ int hodg_elem_stage(const hodg_mesh* mesh, int prec, const void* face_buf, const
     if (a->combine < 0 && !a->res && !a->norm_partial) return HODG_EINVAL;
     g_launches++;
     switch (mesh->d.order) {
-        case 0: return hodg_launch_elem_p0(mesh->d, prec, face_buf, *a, err, S(stream));
-        case 1: return hodg_launch_elem_p1(mesh->d, prec, face_buf, *a, err, S(stream));
-        case 2: return hodg_launch_elem_p2(mesh->d, prec, face_buf, *a, err, S(stream));
-        default: return hodg_launch_elem_p3(mesh->d, prec, face_buf, *a, err, S(stream));
+        case 0: return hodg_launch_elem_p0(mesh->d, prec, buf, *a, err, S(stream), es);
+        case 1: return hodg_launch_elem_p1(mesh->d, prec, buf, *a, err, S(stream), es);
+        case 2: return hodg_launch_elem_p2(mesh->d, prec, buf, *a, err, S(stream), es);
+        default: return hodg_launch_elem_p3(mesh->d, prec, buf, *a, err, S(stream), es);
     }
+}
+
+int hodg_elem_stage(const hodg_mesh* mesh, int prec, const void* face_buf, const hodg_stage_args* a, uint32_t* err,
+                    void* stream) {
+    return elem_stage_impl(mesh, prec, face_buf, a, err, stream, 0);
+}
+
+int hodg_elem_stage_es(const hodg_mesh* mesh, int prec, const void* elem_buf, const hodg_stage_args* a,
+                       uint32_t* err, void* stream) {
+    return elem_stage_impl(mesh, prec, elem_buf, a, err, stream, 1);
+}
+
+int64_t hodg_elem_record_len(const hodg_mesh* mesh, int prec) {
+    if (!mesh || (prec != HODG_PREC_F64 && prec != HODG_PREC_MIXED)) return -1;
+    const int stride = hodg_elem_record_stride(mesh->d.order);
+    const int64_t tile = TILE_TAB[mesh->d.order];
+    // whole tiles plus 16 bytes: the last tile's copy is rounded up to 16 B
+    return (mesh->d.n_elems + tile - 1) / tile * tile * stride + 16;
 }
 
 int hodg_local_dt(const hodg_mesh* mesh, const double* state, double cfl, double* dt_vec_out,

@@ -50,6 +50,13 @@ __host__ __device__ constexpr int hsmem() {
     return sizeof(T) == 8 ? ((hstride<T>() % 4 == 2) ? hstride<T>() : hstride<T>() + 2) : hstride<T>();
 }
 
+// element-slot record block: the 4 face records of an element (5 x NQF
+// values each, slot-major, unpadded) plus one pad value, so the stride is
+// odd (conflict-free per-element smem access) and an E-element tile is a
+// 16-byte multiple (one TMA bulk copy per tile)
+constexpr int HSE = 5 * NQF;
+constexpr int EREC = 4 * HSE + 1;
+
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 __host__ __device__ constexpr size_t cmax(size_t a, size_t b) { return a > b ? a : b; }
 
@@ -121,7 +128,8 @@ struct ElemSmem {
     static constexpr size_t fid = geo + size_t(16) * E * 8;                  // 4 x E int32 (tiled)
     static constexpr size_t red = fid + size_t(4) * E * 4;                   // 10 x E doubles
     static constexpr size_t htile = align16(red + size_t(10) * E * 8);       // 4 x E face records
-    static constexpr size_t sx = align16(htile + size_t(4) * E * hsmem<T>() * sizeof(T));
+    static constexpr size_t sx =
+        align16(htile + cmax(size_t(4) * E * hsmem<T>() * sizeof(T), size_t(E) * EREC * sizeof(T)));
     static constexpr size_t sx_bytes = cmax(size_t(E) * RS * 8, size_t(QC) * E * XS * sizeof(T));
     static constexpr size_t total = sx + sx_bytes;
 };
@@ -141,7 +149,10 @@ __host__ __device__ constexpr size_t elem_smem_bytes() {
 //           across the 5 variables);
 //  phase 2: thread (face, qp) closes boundary faces with the BC state and
 //           evaluates the Roe / LLF flux, writing H[f][v][q] (padded record).
-template <typename T, bool BND>
+//  With ES the records go to the element-slot layout instead: each face's
+//  record is stored in the blocks of both (owned) neighbours, so the element
+//  kernel fetches a tile's records with one contiguous copy.
+template <typename T, bool BND, bool ES>
 __global__ void __launch_bounds__(FACE_THREADS, 4) face_flux_kernel(const hodg_mesh_desc m,
                                                                     const double* __restrict__ state,
                                                                     T* __restrict__ hbuf,
@@ -156,6 +167,7 @@ __global__ void __launch_bounds__(FACE_THREADS, 4) face_flux_kernel(const hodg_m
                            sizeof(double);
     __shared__ double fn[2][FT][3];
     __shared__ int finf[2][FT];
+    __shared__ int fdst[2][FT][2];  // ES: record offsets of the left / right blocks (-1: none)
 
     const int t = threadIdx.x;
     const int side = t / (FT * NG);
@@ -205,6 +217,11 @@ __global__ void __launch_bounds__(FACE_THREADS, 4) face_flux_kernel(const hodg_m
     auto publish = [&](const Meta& mt, int buf) {
         if (side == 0 && g == 0) {
             finf[buf][lf] = ((mt.info >> 4) & 15) | (mt.right >= 0 ? 0x100 : 0);
+            if constexpr (ES) {
+                fdst[buf][lf][0] = mt.elem < m.n_elems ? mt.elem * EREC + (mt.info & 3) * HSE : -1;
+                fdst[buf][lf][1] =
+                    (mt.right >= 0 && mt.right < m.n_elems) ? mt.right * EREC + ((mt.info >> 2) & 3) * HSE : -1;
+            }
             fn[buf][lf][0] = mt.nrm.x;
             fn[buf][lf][1] = mt.nrm.y;
             fn[buf][lf][2] = mt.nrm.z;
@@ -280,6 +297,7 @@ __global__ void __launch_bounds__(FACE_THREADS, 4) face_flux_kernel(const hodg_m
             bool ok[2];
             int64_t fid[2];
             int qv[2];
+            int lfv[2];
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
                 const int p = min(p0 + k * FACE_THREADS, npairs - 1);
@@ -287,6 +305,7 @@ __global__ void __launch_bounds__(FACE_THREADS, 4) face_flux_kernel(const hodg_m
                 const int q = p - lfp * NQF;
                 fid[k] = f0 + lfp;
                 qv[k] = q;
+                lfv[k] = lfp;
                 const int info = finf[buf][lfp];
 #pragma unroll
                 for (int d = 0; d < 3; ++d) n[k][d] = T(fn[buf][lfp][d]);
@@ -325,8 +344,20 @@ __global__ void __launch_bounds__(FACE_THREADS, 4) face_flux_kernel(const hodg_m
 #pragma unroll
                     for (int v = 0; v < 5; ++v) h[k][v] = T(0);
                 }
+                if constexpr (ES) {
+                    const int dl = fdst[buf][lfv[k]][0], dr = fdst[buf][lfv[k]][1];
+                    if (dl >= 0) {
 #pragma unroll
-                for (int v = 0; v < 5; ++v) hbuf[fid[k] * HS + v * NQF + qv[k]] = h[k][v];
+                        for (int v = 0; v < 5; ++v) hbuf[int64_t(dl) + v * NQF + qv[k]] = h[k][v];
+                    }
+                    if (dr >= 0) {
+#pragma unroll
+                        for (int v = 0; v < 5; ++v) hbuf[int64_t(dr) + v * NQF + qv[k]] = h[k][v];
+                    }
+                } else {
+#pragma unroll
+                    for (int v = 0; v < 5; ++v) hbuf[fid[k] * HS + v * NQF + qv[k]] = h[k][v];
+                }
             }
         }
         cur = nxt;
@@ -348,7 +379,9 @@ __global__ void __launch_bounds__(FACE_THREADS, 4) face_flux_kernel(const hodg_m
 //  then the reference mass solve (FP64), RK combination, dt / norm epilogues.
 // Geometry tiles are field-major ([tile][field][E]) so every smem access in
 // the hot phases is unit-stride across the warp.
-template <typename T>
+// ES: the records are in the element-slot layout -- one bulk copy of the
+// tile's record blocks, issued with the state tile, no per-face gather.
+template <typename T, bool ES>
 __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? 4 : 3) elem_stage_kernel(const hodg_mesh_desc m, const T* __restrict__ hbuf,
                                                               const hodg_stage_args a, uint32_t* __restrict__ err) {
     using L = ElemSmem<T>;
@@ -372,10 +405,21 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? 4 : 3) elem_stage_k
         mbar_init(bar + 1, 4 * E);
         mbar_fence_init();
         const uint32_t bs = uint32_t(ne) * RS * 8;
-        mbar_arrive_expect_tx(bar, bs + 16 * E * 8 + 4 * E * 4);
-        bulk_g2s(S, a.us + e0 * RS, bs, bar);
-        bulk_g2s(G, m.egeo + tile * 16 * E, 16 * E * 8, bar);
-        bulk_g2s(FI, m.efaces + tile * 4 * E, 4 * E * 4, bar);
+        if constexpr (ES) {
+            const uint32_t hb = uint32_t(align16(size_t(ne) * EREC * sizeof(T)));
+            mbar_init(bar + 1, 1);
+            mbar_fence_init();
+            mbar_arrive_expect_tx(bar, bs + 16 * E * 8);
+            bulk_g2s(S, a.us + e0 * RS, bs, bar);
+            bulk_g2s(G, m.egeo + tile * 16 * E, 16 * E * 8, bar);
+            mbar_arrive_expect_tx(bar + 1, hb);
+            bulk_g2s(HT, hbuf + e0 * EREC, hb, bar + 1);
+        } else {
+            mbar_arrive_expect_tx(bar, bs + 16 * E * 8 + 4 * E * 4);
+            bulk_g2s(S, a.us + e0 * RS, bs, bar);
+            bulk_g2s(G, m.egeo + tile * 16 * E, 16 * E * 8, bar);
+            bulk_g2s(FI, m.efaces + tile * 4 * E, 4 * E * 4, bar);
+        }
     }
     __syncthreads();
     mbar_wait(bar, 0);
@@ -383,7 +427,7 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? 4 : 3) elem_stage_k
     const int v = t / E;
     const int e = t - v * E;
     // face flux records: thread (s, e) for t < 4E fetches face FI[s][e]
-    if (t < 4 * E) {
+    if (!ES && t < 4 * E) {
         const int ee = t % E;
         if (ee < ne) {
             const int64_t f = FI[t];
@@ -499,9 +543,12 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? 4 : 3) elem_stage_k
 #pragma unroll
         for (int i = 0; i < NB; ++i) accd[i] = double(acc[i]);
         sfor<4>([&](auto s) {
-            const T* hrec = HT + size_t(s * E + e) * HSS + v * NQF;
+            const T* hrec = ES ? HT + size_t(e) * EREC + s * HSE + v * NQF : HT + size_t(s * E + e) * HSS + v * NQF;
             T hq[NQF];
-            if constexpr (sizeof(T) == 8) {
+            if constexpr (ES) {
+#pragma unroll
+                for (int q = 0; q < NQF; ++q) hq[q] = hrec[q];
+            } else if constexpr (sizeof(T) == 8) {
                 // record rows are 16-byte aligned: 128-bit loads on aligned pairs
                 if ((v * NQF) & 1) ld_rec<NQF, 1>(hrec, hq);
                 else ld_rec<NQF, 0>(hrec, hq);
@@ -723,13 +770,13 @@ __global__ void modal_transform_kernel(const hodg_mesh_desc m, int to_reference,
 namespace hodg {
 namespace HODG_CAT(ord, ORDER) {
 
-template <typename T, bool BND>
+template <typename T, bool BND, bool ES>
 static int launch_face_k(const hodg_mesh_desc& m, const double* state, void* hbuf, uint32_t* err, cudaStream_t st,
                          int64_t fb, int64_t fe) {
     const size_t sm = face_smem_bytes<T>();
     static bool attr = false;
     if (!attr) {
-        if (cudaFuncSetAttribute(face_flux_kernel<T, BND>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)) !=
+        if (cudaFuncSetAttribute(face_flux_kernel<T, BND, ES>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)) !=
             cudaSuccess)
             return HODG_ECUDA;
         attr = true;
@@ -739,13 +786,13 @@ static int launch_face_k(const hodg_mesh_desc& m, const double* state, void* hbu
         int dev = 0, sms = 0, per_sm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, face_flux_kernel<T, BND>, FACE_THREADS, sm);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, face_flux_kernel<T, BND, ES>, FACE_THREADS, sm);
         grid_cap = sms * (per_sm > 0 ? per_sm : 1);
     }
     const int64_t ntiles = (fe - fb + FT - 1) / FT;
     const int64_t nblk = ntiles < grid_cap ? ntiles : grid_cap;  // persistent CTAs loop over tiles
     if (nblk > 0)
-        face_flux_kernel<T, BND>
+        face_flux_kernel<T, BND, ES>
             <<<unsigned(nblk), FACE_THREADS, sm, st>>>(m, state, static_cast<T*>(hbuf), err, fb, fe);
     return cudaGetLastError() == cudaSuccess ? HODG_OK : HODG_ECUDA;
 }
@@ -754,26 +801,35 @@ static int launch_face_k(const hodg_mesh_desc& m, const double* state, void* hbu
 // state code in the kernel)
 template <typename T>
 static int launch_face(const hodg_mesh_desc& m, const double* state, void* hbuf, uint32_t* err, cudaStream_t st,
-                       int64_t fb, int64_t fe, int interior_only) {
-    return interior_only ? launch_face_k<T, false>(m, state, hbuf, err, st, fb, fe)
-                         : launch_face_k<T, true>(m, state, hbuf, err, st, fb, fe);
+                       int64_t fb, int64_t fe, int interior_only, int es) {
+    if (es)
+        return interior_only ? launch_face_k<T, false, true>(m, state, hbuf, err, st, fb, fe)
+                             : launch_face_k<T, true, true>(m, state, hbuf, err, st, fb, fe);
+    return interior_only ? launch_face_k<T, false, false>(m, state, hbuf, err, st, fb, fe)
+                         : launch_face_k<T, true, false>(m, state, hbuf, err, st, fb, fe);
 }
 
-template <typename T>
-static int launch_elem(const hodg_mesh_desc& m, const void* hbuf, const hodg_stage_args& a, uint32_t* err,
-                       cudaStream_t st) {
+template <typename T, bool ES>
+static int launch_elem_k(const hodg_mesh_desc& m, const void* hbuf, const hodg_stage_args& a, uint32_t* err,
+                         cudaStream_t st) {
     const size_t sm = elem_smem_bytes<T>();
     static bool attr = false;
     if (!attr) {
-        if (cudaFuncSetAttribute(elem_stage_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)) !=
+        if (cudaFuncSetAttribute(elem_stage_kernel<T, ES>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)) !=
             cudaSuccess)
             return HODG_ECUDA;
         attr = true;
     }
     const int64_t nblk = (m.n_elems + E - 1) / E;
     if (nblk > 0)
-        elem_stage_kernel<T><<<unsigned(nblk), ETHREADS, sm, st>>>(m, static_cast<const T*>(hbuf), a, err);
+        elem_stage_kernel<T, ES><<<unsigned(nblk), ETHREADS, sm, st>>>(m, static_cast<const T*>(hbuf), a, err);
     return cudaGetLastError() == cudaSuccess ? HODG_OK : HODG_ECUDA;
+}
+
+template <typename T>
+static int launch_elem(const hodg_mesh_desc& m, const void* hbuf, const hodg_stage_args& a, uint32_t* err,
+                       cudaStream_t st, int es) {
+    return es ? launch_elem_k<T, true>(m, hbuf, a, err, st) : launch_elem_k<T, false>(m, hbuf, a, err, st);
 }
 
 }  // namespace HODG_CAT(ord, ORDER)
@@ -781,18 +837,21 @@ static int launch_elem(const hodg_mesh_desc& m, const void* hbuf, const hodg_sta
 
 extern "C++" {
 int HODG_CAT(hodg_launch_face_p, ORDER)(const hodg_mesh_desc& m, int prec, const double* state, void* hbuf,
-                                         uint32_t* err, cudaStream_t st, int64_t fb, int64_t fe, int interior) {
+                                         uint32_t* err, cudaStream_t st, int64_t fb, int64_t fe, int interior,
+                                         int es) {
     using namespace hodg::HODG_CAT(ord, ORDER);
-    return prec == HODG_PREC_MIXED ? launch_face<float>(m, state, hbuf, err, st, fb, fe, interior)
-                                   : launch_face<double>(m, state, hbuf, err, st, fb, fe, interior);
+    return prec == HODG_PREC_MIXED ? launch_face<float>(m, state, hbuf, err, st, fb, fe, interior, es)
+                                   : launch_face<double>(m, state, hbuf, err, st, fb, fe, interior, es);
 }
 
 int HODG_CAT(hodg_launch_elem_p, ORDER)(const hodg_mesh_desc& m, int prec, const void* hbuf,
-                                         const hodg_stage_args& a, uint32_t* err, cudaStream_t st) {
+                                         const hodg_stage_args& a, uint32_t* err, cudaStream_t st, int es) {
     using namespace hodg::HODG_CAT(ord, ORDER);
-    return prec == HODG_PREC_MIXED ? launch_elem<float>(m, hbuf, a, err, st)
-                                   : launch_elem<double>(m, hbuf, a, err, st);
+    return prec == HODG_PREC_MIXED ? launch_elem<float>(m, hbuf, a, err, st, es)
+                                   : launch_elem<double>(m, hbuf, a, err, st, es);
 }
+
+int HODG_CAT(hodg_elem_record_stride_p, ORDER)() { return hodg::HODG_CAT(ord, ORDER)::EREC; }
 
 int HODG_CAT(hodg_launch_dt_p, ORDER)(const hodg_mesh_desc& m, const double* state, double cfl, double* dt_vec,
                                        unsigned long long* dt_min, uint32_t* err, cudaStream_t st) {

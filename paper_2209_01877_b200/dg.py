@@ -150,6 +150,7 @@ class Discretization:
         self.err = torch.empty(4, dtype=torch.int32, device=self.device)
         self.nblk = int(self.L.hodg_stage_blocks(h, 64))
         self._hbuf = {}
+        self._ebuf = {}
         self._scratch = torch.empty(max(self.nblk, (self.n + 255) // 256) * 5 + 1024, dtype=torch.float64,
                                     device=self.device)
 
@@ -169,6 +170,17 @@ class Discretization:
             hs = int(self.L.hodg_face_record_stride(self.order, prec))
             b = torch.zeros((self.nf, hs), dtype=dt, device=self.device)
             self._hbuf[prec] = b
+        return b
+
+    def elem_buffer(self, prec):
+        """Element-slot record buffer (include/hodg_b200.h: hodg_face_flux_range_es):
+        1-D, so face_flux / stage select the element-slot kernels by shape."""
+        torch = _torch()
+        b = self._ebuf.get(prec)
+        if b is None:
+            dt = torch.float32 if prec == _lib.PREC_MIXED else torch.float64
+            b = torch.zeros(int(self.L.hodg_elem_record_len(self.handle, prec)), dtype=dt, device=self.device)
+            self._ebuf[prec] = b
         return b
 
     def new_state(self, rows=None):
@@ -224,13 +236,15 @@ class Discretization:
         for lo, hi, interior in ((0, b0, 1), (b0, b1, 0), (b1, self.nf, 1)):
             lo, hi = max(lo, f_begin), min(hi, f_end)
             if hi > lo:
-                _lib.check(self.L.hodg_face_flux_range(self.handle, prec, _lib.ptr(rows), _lib.ptr(hbuf), int(lo),
+                fn = self.L.hodg_face_flux_range_es if hbuf.dim() == 1 else self.L.hodg_face_flux_range
+                _lib.check(fn(self.handle, prec, _lib.ptr(rows), _lib.ptr(hbuf), int(lo),
                                                        int(hi), interior, _lib.ptr(self.err),
                                                        _lib.stream_ptr(stream)), "hodg_face_flux_range")
         return hbuf
 
     def stage(self, prec, hbuf, args: _lib.StageArgs, stream=None):
-        _lib.check(self.L.hodg_elem_stage(self.handle, prec, _lib.ptr(hbuf), C.byref(args), _lib.ptr(self.err),
+        fn = self.L.hodg_elem_stage_es if hbuf.dim() == 1 else self.L.hodg_elem_stage
+        _lib.check(fn(self.handle, prec, _lib.ptr(hbuf), C.byref(args), _lib.ptr(self.err),
                                           _lib.stream_ptr(stream)), "hodg_elem_stage")
 
     def residual_rows(self, rows, hbuf, prec, res=None):

@@ -61,9 +61,12 @@ class MachineModel:
             raise ValueError("machine peaks must be positive")
 
 
-# measured on this pool's B200s: DFMA 36.3 TFLOP/s (profiles/fp64_peaks.md),
-# copy bandwidth 6551 GB/s (MEASURED_PEAKS.json)
-B200 = MachineModel("b200-fp64", 36.3e12, 6551.4e9)
+# measured on this pool's B200s: DFMA 36.3 TFLOP/s = 18.15 T FP64-pipe
+# instructions/s (profiles/fp64_peaks.md; DMMA shares the same budget), copy
+# bandwidth 6551 GB/s (MEASURED_PEAKS.json).  count_flops_and_bytes counts
+# an FMA as one operation, so the machine model's peak is in the same unit.
+FP64_PIPE_OPS_PER_S = 36.3e12 / 2
+B200 = MachineModel("b200-fp64", FP64_PIPE_OPS_PER_S, 6551.4e9)
 
 
 def dual_phase(run_fn, n1: int, n2: int) -> PerfSample:

@@ -189,8 +189,11 @@ class Stepper:
     """
 
     def __init__(self, disc: Discretization, scheme="rk3", prec=_lib.PREC_F64, dt_mode="global", cfl=0.3,
-                 log_norms=True, use_graph=True):
+                 log_norms=True, use_graph=True, layout="auto"):
         torch = _torch()
+        if layout not in ("auto", "elem", "face"):
+            raise ValueError(f"unknown record layout {layout!r}")
+        self.layout = layout
         if scheme not in SCHEMES:
             raise ValueError(f"unknown scheme {scheme!r}")
         if dt_mode not in ("local", "global"):
@@ -201,7 +204,7 @@ class Stepper:
         dev = disc.device
         self.A = disc.new_state()
         self.B = disc.new_state()
-        self.hbuf = disc.face_buffer(prec)
+        self.hbuf = self._records(prec)
         self.slots = torch.full((2,), INF_BITS, dtype=torch.int64, device=dev)
         self.dtv = [torch.zeros(disc.n, dtype=torch.float64, device=dev) for _ in range(2)]
         self.partial = torch.zeros((disc.nblk, 5), dtype=torch.float64, device=dev)
@@ -238,6 +241,14 @@ class Stepper:
         return min_reduce(self.dtv[self.parity])
 
     # -- one step ----------------------------------------------------------
+    def _records(self, prec):
+        """Face flux record buffer: the element-slot layout (one bulk copy per
+        element tile, but two record stores per face) or the face-ordered one.
+        "auto" takes the faster per precision on the B200 (profiles/r1k_summary.md):
+        element-slot for mixed precision, face-ordered for FP64."""
+        use_elem = self.layout == "elem" or (self.layout == "auto" and prec == _lib.PREC_MIXED)
+        return self.disc.elem_buffer(prec) if use_elem else self.disc.face_buffer(prec)
+
     def _stage_args(self, k, parity):
         d = self.disc
         combine, a, b = SCHEMES[self.scheme][k]
@@ -437,7 +448,7 @@ def run(config: RunConfig, mesh: TetMesh | None = None) -> RunArtifacts:
         want = _lib.PREC_MIXED if bits == 32 else _lib.PREC_F64
         if want != stepper.prec:
             stepper.prec = want
-            stepper.hbuf = disc.face_buffer(want)
+            stepper.hbuf = stepper._records(want)
             stepper._graphs.clear()
         log = config.log_every and (it % config.log_every == 0 or it == config.max_iterations - 1)
         dt_log = stepper.dt_value() if log else None

@@ -235,11 +235,36 @@ def test_partitioned_residual_bitwise_on_one_gpu(P, nparts):
                            n_elems=part.n_owned)
         gl = torch.as_tensor(np.concatenate([part.owned, part.ghosts]), device="cuda")
         rows = rows_g.index_select(0, gl).contiguous()  # owned + ghost rows (the halo)
-        hb = d.face_buffer(64)
-        d.reset_errors()
-        d.face_flux(rows, 64, hb, f_begin=0, f_end=part.n_inner_faces)
-        d.face_flux(rows, 64, hb, f_begin=part.n_inner_faces, f_end=d.nf)
-        res = d.residual_rows(rows, hb, 64, res=d.new_state())
-        d.raise_errors()
         own = torch.as_tensor(part.owned, device="cuda")
-        assert torch.equal(res[: part.n_owned], ref.index_select(0, own)), r
+        for hb in (d.face_buffer(64), d.elem_buffer(64)):  # both record layouts
+            d.reset_errors()
+            d.face_flux(rows, 64, hb, f_begin=0, f_end=part.n_inner_faces)
+            d.face_flux(rows, 64, hb, f_begin=part.n_inner_faces, f_end=d.nf)
+            res = d.residual_rows(rows, hb, 64, res=d.new_state())
+            d.raise_errors()
+            assert torch.equal(res[: part.n_owned], ref.index_select(0, own)), (r, hb.dim())
+
+
+@pytest.mark.parametrize("order", [0, 1, 2, 3])
+@pytest.mark.parametrize("prec", [64, 32])
+def test_element_slot_layout_bitwise(P, order, prec):
+    """The stepper's element-slot record path (hodg_face_flux_range_es +
+    hodg_elem_stage_es) gives the same residual bits as the face-ordered
+    path: same values, same summation order, different placement."""
+    import torch
+
+    from paper_2209_01877_b200.dg import _get_disc
+
+    for name, m in meshes():
+        disc_o, c = oracle_state(m, order)
+        gas, geo, bcs = gpu_setup(P, m, order)
+        d = _get_disc(m, geo, gas, bcs)
+        rows = d.to_reference(torch.from_numpy(c).cuda())
+        p = P._lib.PREC_F64 if prec == 64 else P._lib.PREC_MIXED
+        d.reset_errors()
+        ref = d.residual_rows(rows, d.face_flux(rows, p, d.face_buffer(p)), p)
+        eb = d.elem_buffer(p)
+        eb.fill_(float("nan"))  # every slot must be written
+        got = d.residual_rows(rows, d.face_flux(rows, p, eb), p)
+        d.raise_errors()
+        assert torch.equal(got, ref), (name, order, prec)
