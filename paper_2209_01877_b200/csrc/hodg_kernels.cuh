@@ -19,7 +19,10 @@ namespace hodg {
 namespace HODG_CAT(ord, ORDER) {
 
 constexpr int RS = (5 * NB + 1) & ~1;        // state row stride (doubles)
-constexpr int NG = (NQF > 1) ? 2 : 1;        // face qp groups per side thread
+#ifndef HODG_NG3
+#define HODG_NG3 4
+#endif
+constexpr int NG = (NQF > 7) ? HODG_NG3 : ((NQF > 1) ? 2 : 1);  // face qp groups per side thread
 constexpr int QPT = (NQF + NG - 1) / NG;     // face qps per phase-1 thread
 constexpr int FACE_THREADS = 128;
 constexpr int FT = FACE_THREADS / (2 * NG);  // faces per CTA (32 for P1-P3)
