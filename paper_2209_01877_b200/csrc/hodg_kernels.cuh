@@ -34,11 +34,14 @@ constexpr int E = (ORDER >= 3) ? 16 : (ORDER == 2 ? 32 : 64);  // elements per C
 #endif
 constexpr int ETHREADS = 5 * E;
 constexpr int XS = 15;                        // smem slot per (element, qp): 5 traces -> 15 contravariant fluxes
-#ifdef HODG_QC2_OVERRIDE
-constexpr int QC = (NQV <= 8) ? NQV : (ORDER == 2 ? HODG_QC2_OVERRIDE : 8);
-#else
-constexpr int QC = (NQV <= 8) ? NQV : (ORDER == 2 ? 7 : 8);  // volume qps per chunk (bounds the X buffer)
+#ifndef HODG_QC2
+#define HODG_QC2 7
 #endif
+#ifndef HODG_QC3
+#define HODG_QC3 6
+#endif
+// volume qps per chunk (bounds the X buffer; at P3 small enough for 4 CTAs/SM)
+constexpr int QC = (NQV <= 8) ? NQV : (ORDER == 2 ? HODG_QC2 : HODG_QC3);
 constexpr int NCH = (NQV + QC - 1) / QC;
 
 // padded per-face record of the face flux buffer: 5 x NQF values rounded up
