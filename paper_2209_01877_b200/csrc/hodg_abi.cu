@@ -15,6 +15,7 @@
     int hodg_launch_elem_p##P(const hodg_mesh_desc&, int, const void*, const hodg_stage_args&, uint32_t*,      \
                               cudaStream_t, int);                                                              \
     int hodg_elem_record_stride_p##P();                                                                        \
+    int hodg_elem_tile_p##P();                                                                                 \
     int hodg_launch_dt_p##P(const hodg_mesh_desc&, const double*, double, double*, unsigned long long*,        \
                             uint32_t*, cudaStream_t);                                                          \
     int hodg_launch_modal_p##P(const hodg_mesh_desc&, int, const double*, double*, cudaStream_t);             \
@@ -43,7 +44,6 @@ namespace {
 constexpr int NB_TAB[4] = {1, 4, 10, 20};
 constexpr int NQV_TAB[4] = {1, 4, 14, 24};
 constexpr int NQF_TAB[4] = {1, 6, 7, 15};
-constexpr int TILE_TAB[4] = {64, 64, 32, 16};  // elements per CTA (hodg_kernels.cuh: E)
 
 inline int rs_of(int p) { return (5 * NB_TAB[p] + 1) & ~1; }
 
@@ -153,7 +153,15 @@ int hodg_state_row_stride(int order) { return (order < 0 || order > 3) ? -1 : rs
 int hodg_n_basis(int order) { return (order < 0 || order > 3) ? -1 : NB_TAB[order]; }
 int hodg_n_face_points(int order) { return (order < 0 || order > 3) ? -1 : NQF_TAB[order]; }
 int hodg_n_vol_points(int order) { return (order < 0 || order > 3) ? -1 : NQV_TAB[order]; }
-int hodg_elem_tile(int order) { return (order < 0 || order > 3) ? -1 : TILE_TAB[order]; }
+int hodg_elem_tile(int order) {
+    switch (order) {
+        case 0: return hodg_elem_tile_p0();
+        case 1: return hodg_elem_tile_p1();
+        case 2: return hodg_elem_tile_p2();
+        case 3: return hodg_elem_tile_p3();
+        default: return -1;
+    }
+}
 int hodg_elem_record_stride(int order) {
     switch (order) {
         case 0: return hodg_elem_record_stride_p0();
@@ -263,7 +271,7 @@ int hodg_elem_stage_es(const hodg_mesh* mesh, int prec, const void* elem_buf, co
 int64_t hodg_elem_record_len(const hodg_mesh* mesh, int prec) {
     if (!mesh || (prec != HODG_PREC_F64 && prec != HODG_PREC_MIXED)) return -1;
     const int stride = hodg_elem_record_stride(mesh->d.order);
-    const int64_t tile = TILE_TAB[mesh->d.order];
+    const int64_t tile = hodg_elem_tile(mesh->d.order);
     // whole tiles plus 16 bytes: the last tile's copy is rounded up to 16 B
     return (mesh->d.n_elems + tile - 1) / tile * tile * stride + 16;
 }
@@ -304,7 +312,7 @@ int hodg_residual_l2(const hodg_mesh* mesh, const double* res, double* scratch, 
     const int64_t nblk = (n + RT - 1) / RT;
     g_launches += 2;
     const int p = mesh->d.order;
-    norm_partial_kernel<<<unsigned(nblk), RT, 0, S(stream)>>>(res, mesh->d.egeo, n, rs_of(p), NB_TAB[p], TILE_TAB[p],
+    norm_partial_kernel<<<unsigned(nblk), RT, 0, S(stream)>>>(res, mesh->d.egeo, n, rs_of(p), NB_TAB[p], hodg_elem_tile(p),
                                                                scratch);
     norm_finalize_kernel<<<1, RT, 0, S(stream)>>>(scratch, nblk, out5);
     return cudaGetLastError() == cudaSuccess ? HODG_OK : HODG_ECUDA;

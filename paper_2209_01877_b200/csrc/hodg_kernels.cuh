@@ -27,12 +27,24 @@ constexpr int QPT = (NQF + NG - 1) / NG;     // face qps per phase-1 thread
 constexpr int FACE_THREADS = 128;
 constexpr int FT = FACE_THREADS / (2 * NG);  // faces per CTA (32 for P1-P3)
 constexpr int FBS = NQF * NB + 1;            // padded per-slot stride of the smem trace table
-#ifdef HODG_E2_OVERRIDE
-constexpr int E = (ORDER >= 3) ? 16 : (ORDER == 2 ? HODG_E2_OVERRIDE : 64);
-#else
-constexpr int E = (ORDER >= 3) ? 16 : (ORDER == 2 ? 32 : 64);  // elements per CTA
+// element kernel: E elements per CTA, thread (v, h, e) -- variable v, basis
+// part h of H (each thread owns NB/H basis functions of its (v, e); H > 1
+// halves the per-thread registers at P3 so twice the warps fit per SM)
+#ifndef HODG_H2
+#define HODG_H2 1
 #endif
-constexpr int ETHREADS = 5 * E;
+#ifndef HODG_H3
+#define HODG_H3 2
+#endif
+constexpr int H = (ORDER == 3) ? HODG_H3 : (ORDER == 2 ? HODG_H2 : 1);
+#ifndef HODG_E2
+#define HODG_E2 32
+#endif
+constexpr int E = (ORDER >= 3) ? (H > 1 ? 32 : 16) : (ORDER == 2 ? HODG_E2 : 64);  // elements per CTA
+constexpr int NH = NB / H;
+static_assert(NB % H == 0 && (H == 1 || E >= 32) && 5 * H <= 15, "basis split layout");
+constexpr int ETHREADS = 5 * E * H;
+constexpr int EMINB = H > 1 ? 2 : 3;  // CTAs per SM the FP64 element kernel is register-budgeted for
 constexpr int XS = 15;                        // smem slot per (element, qp): 5 traces -> 15 contravariant fluxes
 #ifndef HODG_QC2
 #define HODG_QC2 7
@@ -127,22 +139,37 @@ __host__ __device__ constexpr size_t face_smem_bytes() {
 }
 
 // element kernel shared memory carve-up
-template <typename T>
+template <typename T, bool ES>
 struct ElemSmem {
     static constexpr size_t bar = 0;                                         // 2 mbarriers
     static constexpr size_t geo = 16;                                        // 16 x E doubles (tiled)
     static constexpr size_t fid = geo + size_t(16) * E * 8;                  // 4 x E int32 (tiled)
-    static constexpr size_t red = fid + size_t(4) * E * 4;                   // 10 x E doubles
-    static constexpr size_t htile = align16(red + size_t(10) * E * 8);       // 4 x E face records
-    static constexpr size_t sx =
-        align16(htile + cmax(size_t(4) * E * hsmem<T>() * sizeof(T), size_t(E) * EREC * sizeof(T)));
+    static constexpr size_t red = fid + size_t(4) * E * 4;                   // (5 + 5H) x E doubles
+    static constexpr size_t htile = align16(red + size_t(5 + 5 * H) * E * 8);  // 4 x E face records
+    static constexpr size_t hbytes = ES ? size_t(E) * EREC * sizeof(T) : size_t(4) * E * hsmem<T>() * sizeof(T);
+    static constexpr size_t sx = align16(htile + hbytes);
     static constexpr size_t sx_bytes = cmax(size_t(E) * RS * 8, size_t(QC) * E * XS * sizeof(T));
     static constexpr size_t total = sx + sx_bytes;
+    // H > 1: the residual exchange of the mass solve reuses the record tile
+    static_assert(H == 1 || hbytes >= size_t(5) * E * NB * 8, "solve exchange fits the record tile");
 };
 
-template <typename T>
+template <typename T, bool ES>
 __host__ __device__ constexpr size_t elem_smem_bytes() {
-    return ElemSmem<T>::total;
+    return ElemSmem<T, ES>::total;
+}
+
+// h (runtime, warp-uniform) -> compile-time constant
+template <typename F>
+__device__ __forceinline__ void hsel(int h, F&& f) {
+    if constexpr (H == 1) {
+        f(std::integral_constant<int, 0>{});
+    } else if constexpr (H == 2) {
+        if (h == 0) f(std::integral_constant<int, 0>{});
+        else f(std::integral_constant<int, 1>{});
+    } else {
+        static_assert(H <= 2, "basis split of 1 or 2");
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -388,19 +415,22 @@ __global__ void __launch_bounds__(FACE_THREADS, 4) face_flux_kernel(const hodg_m
 // ES: the records are in the element-slot layout -- one bulk copy of the
 // tile's record blocks, issued with the state tile, no per-face gather.
 template <typename T, bool ES>
-__global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? 4 : 3) elem_stage_kernel(const hodg_mesh_desc m, const T* __restrict__ hbuf,
-                                                              const hodg_stage_args a, uint32_t* __restrict__ err) {
-    using L = ElemSmem<T>;
+__global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : 4) : EMINB)
+    elem_stage_kernel(const hodg_mesh_desc m, const T* __restrict__ hbuf, const hodg_stage_args a,
+                      uint32_t* __restrict__ err) {
+    using L = ElemSmem<T, ES>;
     constexpr int HS = hstride<T>();
     constexpr int HSS = hsmem<T>();
     extern __shared__ __align__(16) unsigned char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::bar);
     double* G = reinterpret_cast<double*>(smem + L::geo);
     int32_t* FI = reinterpret_cast<int32_t*>(smem + L::fid);
-    double* RED = reinterpret_cast<double*>(smem + L::red);  // [0, 5E): norm terms, [5E, 10E): cell means
+    // [0, 5E): norm terms; [5E + 5E h, 10E + 5E h): cell-mean partials of basis part h
+    double* RED = reinterpret_cast<double*>(smem + L::red);
     T* HT = reinterpret_cast<T*>(smem + L::htile);
-    double* S = reinterpret_cast<double*>(smem + L::sx);  // state tile, later the output tile
-    T* X = reinterpret_cast<T*>(smem + L::sx);            // per-chunk trace / flux slots
+    double* Z = reinterpret_cast<double*>(smem + L::htile);  // H > 1: residual exchange (after the gather)
+    double* S = reinterpret_cast<double*>(smem + L::sx);     // state tile, later the output tile
+    T* X = reinterpret_cast<T*>(smem + L::sx);               // per-chunk trace / flux slots
     const int t = threadIdx.x;
     const int64_t tile = blockIdx.x;
     const int64_t e0 = tile * E;
@@ -408,13 +438,11 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? 4 : 3) elem_stage_k
     if (t == 0) {
         if (a.dt_reset && blockIdx.x == 0) *a.dt_reset = 0x7FF0000000000000ull;
         mbar_init(bar, 1);
-        mbar_init(bar + 1, 4 * E);
+        mbar_init(bar + 1, ES ? 1 : 4 * E);
         mbar_fence_init();
         const uint32_t bs = uint32_t(ne) * RS * 8;
         if constexpr (ES) {
             const uint32_t hb = uint32_t(align16(size_t(ne) * EREC * sizeof(T)));
-            mbar_init(bar + 1, 1);
-            mbar_fence_init();
             mbar_arrive_expect_tx(bar, bs + 16 * E * 8);
             bulk_g2s(S, a.us + e0 * RS, bs, bar);
             bulk_g2s(G, m.egeo + tile * 16 * E, 16 * E * 8, bar);
@@ -430,8 +458,10 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? 4 : 3) elem_stage_k
     __syncthreads();
     mbar_wait(bar, 0);
 
-    const int v = t / E;
-    const int e = t - v * E;
+    // thread (v, h, e): e fastest, so h is warp-uniform (E >= 32 when H > 1)
+    const int e = t % E;
+    const int h = (t / E) % H;
+    const int v = t / (E * H);
     // face flux records: thread (s, e) for t < 4E fetches face FI[s][e]
     if (!ES && t < 4 * E) {
         const int ee = t % E;
@@ -447,44 +477,50 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? 4 : 3) elem_stage_k
     const int64_t gid = e0 + e;
     const bool live = e < ne;
     const bool need_u0 = a.combine == 1 || (a.combine == 0 && a.a != 0.0);
-    double c[NB];
-    double u0r[(ORDER <= 2) ? NB : 1];
+    const int jb = h * NH;  // first basis function of this thread's part
+    double c[NH];
+    double u0r[(ORDER <= 2) ? NH : 1];
     if (live) {
-        if constexpr ((NB % 2) == 0) {
+        if constexpr (H == 1 && (NB % 2) == 0) {
             ld_row(S + e * RS + v * NB, c);  // rows 16-byte aligned when NB is even
         } else {
 #pragma unroll
-            for (int i = 0; i < NB; ++i) c[i] = S[e * RS + v * NB + i];
+            for (int i = 0; i < NH; ++i) c[i] = S[e * RS + v * NB + jb + i];
         }
         if constexpr (ORDER <= 2) {
             if (need_u0) {
-                if constexpr ((NB % 2) == 0) {
+                if constexpr (H == 1 && (NB % 2) == 0) {
                     ld_row(a.u0 + gid * RS + v * NB, u0r);
                 } else {
 #pragma unroll
-                    for (int i = 0; i < NB; ++i) u0r[i] = a.u0[gid * RS + v * NB + i];
+                    for (int i = 0; i < NH; ++i) u0r[i] = a.u0[gid * RS + v * NB + jb + i];
                 }
             }
         }
     }
     __syncthreads();  // state tile consumed: the region now holds X
 
-    T acc[NB];
+    T acc[NH];
 #pragma unroll
-    for (int i = 0; i < NB; ++i) acc[i] = T(0);
-    T ji[9];
+    for (int i = 0; i < NH; ++i) acc[i] = T(0);
+    T ji[H == 1 ? 9 : 1];
+    if constexpr (H == 1) {
 #pragma unroll
-    for (int k = 0; k < 9; ++k) ji[k] = T(G[k * E + e]);
+        for (int k = 0; k < 9; ++k) ji[k] = T(G[k * E + e]);
+    }
     const T gam = T(m.gamma);
     sfor<NCH>([&](auto ch) {
         constexpr int q0 = ch * QC;
         constexpr int nq = (NQV - q0) < QC ? (NQV - q0) : QC;
-        // phase A
+        // phase A: traces of variable v (H > 1: partial sums of this part,
+        // added in phase B in part order)
         if (live) {
-            sfor<nq>([&](auto qq) {
-                T u = T(0);
-                sfor<NB>([&](auto i) { u += TAB(VB, T, (q0 + qq) * NB + i) * T(c[i]); });
-                X[(qq * E + e) * XS + v] = u;
+            hsel(h, [&](auto hc) {
+                sfor<nq>([&](auto qq) {
+                    T u = T(0);
+                    sfor<NH>([&](auto i) { u += TAB(VB, T, (q0 + qq) * NB + hc * NH + i) * T(c[i]); });
+                    X[(qq * E + e) * XS + hc * 5 + v] = u;
+                });
             });
         }
         __syncthreads();
@@ -497,6 +533,12 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? 4 : 3) elem_stage_k
             T U[5];
 #pragma unroll
             for (int k = 0; k < 5; ++k) U[k] = sl[k];
+            if constexpr (H > 1) {
+#pragma unroll
+                for (int hh = 1; hh < H; ++hh)
+#pragma unroll
+                    for (int k = 0; k < 5; ++k) U[k] += sl[hh * 5 + k];
+            }
             T u, vv, w;
             const T pr = (U[0] > T(0)) ? prim(U, gam, u, vv, w) : T(-1);
             if (!(pr > T(0))) {
@@ -505,36 +547,52 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? 4 : 3) elem_stage_k
                 for (int k = 0; k < XS; ++k) sl[k] = T(0);
                 continue;
             }
-            // physical flux F[d][var]; the reference-frame map J^-1 F is
-            // applied per variable in phase C (balanced across threads)
+            // physical flux F[d][var]
             const T Hs = U[4] + pr;
-            sl[0] = U[1];
-            sl[1] = U[1] * u + pr;
-            sl[2] = U[1] * vv;
-            sl[3] = U[1] * w;
-            sl[4] = Hs * u;
-            sl[5] = U[2];
-            sl[6] = U[2] * u;
-            sl[7] = U[2] * vv + pr;
-            sl[8] = U[2] * w;
-            sl[9] = Hs * vv;
-            sl[10] = U[3];
-            sl[11] = U[3] * u;
-            sl[12] = U[3] * vv;
-            sl[13] = U[3] * w + pr;
-            sl[14] = Hs * w;
+            T F[15] = {U[1], U[1] * u + pr, U[1] * vv, U[1] * w, Hs * u,
+                       U[2], U[2] * u, U[2] * vv + pr, U[2] * w, Hs * vv,
+                       U[3], U[3] * u, U[3] * vv, U[3] * w + pr, Hs * w};
+            if constexpr (H == 1) {
+                // the reference-frame map J^-1 F is applied per variable in
+                // phase C (balanced across threads)
+#pragma unroll
+                for (int k = 0; k < 15; ++k) sl[k] = F[k];
+            } else {
+                // H > 1: J^-1 F here (phase C threads hold no J^-1)
+                T jj[9];
+#pragma unroll
+                for (int k = 0; k < 9; ++k) jj[k] = T(G[k * E + ee]);
+#pragma unroll
+                for (int d = 0; d < 3; ++d)
+#pragma unroll
+                    for (int var = 0; var < 5; ++var)
+                        sl[d * 5 + var] = jj[3 * d] * F[var] + jj[3 * d + 1] * F[5 + var] + jj[3 * d + 2] * F[10 + var];
+            }
         }
         __syncthreads();
-        // phase C (volume): contravariant flux of variable v, J^-1 F
+        // phase C (volume): contravariant flux of variable v against the
+        // weighted derivative table, this part's basis functions
         if (live) {
-            sfor<nq>([&](auto qq) {
-                const T* sl = X + (qq * E + e) * XS;
-                const T fx = sl[v], fy = sl[5 + v], fz = sl[10 + v];
-                const T fd[3] = {ji[0] * fx + ji[1] * fy + ji[2] * fz, ji[3] * fx + ji[4] * fy + ji[5] * fz,
-                                 ji[6] * fx + ji[7] * fy + ji[8] * fz};
-                sfor<NB>([&](auto i) {
-                    sfor<3>([&](auto d) {
-                        if constexpr (expt(i, d) > 0) acc[i] += TAB(VD, T, ((q0 + qq) * NB + i) * 3 + d) * fd[d];
+            hsel(h, [&](auto hc) {
+                sfor<nq>([&](auto qq) {
+                    const T* sl = X + (qq * E + e) * XS;
+                    T fd[3];
+                    if constexpr (H == 1) {
+                        const T fx = sl[v], fy = sl[5 + v], fz = sl[10 + v];
+                        fd[0] = ji[0] * fx + ji[1] * fy + ji[2] * fz;
+                        fd[1] = ji[3] * fx + ji[4] * fy + ji[5] * fz;
+                        fd[2] = ji[6] * fx + ji[7] * fy + ji[8] * fz;
+                    } else {
+                        fd[0] = sl[v];
+                        fd[1] = sl[5 + v];
+                        fd[2] = sl[10 + v];
+                    }
+                    sfor<NH>([&](auto i) {
+                        constexpr int ig = hc * NH + i;
+                        sfor<3>([&](auto d) {
+                            if constexpr (expt(ig, d) > 0)
+                                acc[i] += TAB(VD, T, ((q0 + qq) * NB + ig) * 3 + d) * fd[d];
+                        });
                     });
                 });
             });
@@ -544,105 +602,141 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? 4 : 3) elem_stage_k
 
     // face gather, mass solve, RK update
     mbar_wait(bar + 1, 0);
+    double accd[NH];
     if (live) {
-        double accd[NB];
 #pragma unroll
-        for (int i = 0; i < NB; ++i) accd[i] = double(acc[i]);
-        sfor<4>([&](auto s) {
-            const T* hrec = ES ? HT + size_t(e) * EREC + s * HSE + v * NQF : HT + size_t(s * E + e) * HSS + v * NQF;
-            T hq[NQF];
-            if constexpr (ES) {
+        for (int i = 0; i < NH; ++i) accd[i] = double(acc[i]);
+        hsel(h, [&](auto hc) {
+            sfor<4>([&](auto s) {
+                const T* hrec =
+                    ES ? HT + size_t(e) * EREC + s * HSE + v * NQF : HT + size_t(s * E + e) * HSS + v * NQF;
+                T hq[NQF];
+                if constexpr (ES) {
 #pragma unroll
-                for (int q = 0; q < NQF; ++q) hq[q] = hrec[q];
-            } else if constexpr (sizeof(T) == 8) {
-                // record rows are 16-byte aligned: 128-bit loads on aligned pairs
-                if ((v * NQF) & 1) ld_rec<NQF, 1>(hrec, hq);
-                else ld_rec<NQF, 0>(hrec, hq);
-            } else {
+                    for (int q = 0; q < NQF; ++q) hq[q] = hrec[q];
+                } else if constexpr (sizeof(T) == 8) {
+                    // record rows are 16-byte aligned: 128-bit loads on aligned pairs
+                    if ((v * NQF) & 1) ld_rec<NQF, 1>(hrec, hq);
+                    else ld_rec<NQF, 0>(hrec, hq);
+                } else {
 #pragma unroll
-                for (int q = 0; q < NQF; ++q) hq[q] = hrec[q];
-            }
-            T fa[NB];
+                    for (int q = 0; q < NQF; ++q) hq[q] = hrec[q];
+                }
+                T fa[NH];
 #pragma unroll
-            for (int i = 0; i < NB; ++i) fa[i] = T(0);
-            sfor<NQF>([&](auto q) {
-                sfor<NB>([&](auto i) { fa[i] += TAB(FG, T, (s * NQF + q) * NB + i) * hq[q]; });
+                for (int i = 0; i < NH; ++i) fa[i] = T(0);
+                sfor<NQF>([&](auto q) {
+                    sfor<NH>([&](auto i) { fa[i] += TAB(FG, T, (s * NQF + q) * NB + hc * NH + i) * hq[q]; });
+                });
+                const double fc = G[(9 + s) * E + e];
+#pragma unroll
+                for (int i = 0; i < NH; ++i) accd[i] -= fc * double(fa[i]);
             });
-            const double fc = G[(9 + s) * E + e];
-#pragma unroll
-            for (int i = 0; i < NB; ++i) accd[i] -= fc * double(fa[i]);
         });
-        double r[NB];
-        sfor<NB>([&](auto j) {
-            double z = 0.0;
-            sfor<NB>([&](auto k) { z += MINV_T[j * NB + k] * accd[k]; });
-            r[j] = z;
+    }
+    double full[H == 1 ? 1 : NB];
+    if constexpr (H > 1) {
+        // assemble the (v, e) residual vector of all parts (records consumed)
+        __syncthreads();
+        if (live) {
+#pragma unroll
+            for (int i = 0; i < NH; ++i) Z[(v * E + e) * NB + jb + i] = accd[i];
+        }
+        __syncthreads();
+        if (live) {
+#pragma unroll
+            for (int k = 0; k < NB; ++k) full[k] = Z[(v * E + e) * NB + k];
+        }
+    }
+    if (live) {
+        double r[NH];
+        hsel(h, [&](auto hc) {
+            sfor<NH>([&](auto j) {
+                double z = 0.0;
+                if constexpr (H == 1) {
+                    sfor<NB>([&](auto k) { z += MINV_T[j * NB + k] * accd[k]; });
+                } else {
+                    sfor<NB>([&](auto k) { z += MINV_T[(hc * NH + j) * NB + k] * full[k]; });
+                }
+                r[j] = z;
+            });
         });
         if (a.res) {
 #pragma unroll
-            for (int j = 0; j < NB; ++j) a.res[gid * RS + v * NB + j] = r[j];
+            for (int j = 0; j < NH; ++j) a.res[gid * RS + v * NB + jb + j] = r[j];
         }
-        if (a.norm_partial) RED[v * E + e] = G[14 * E + e] * r[0] * r[0];
+        if (a.norm_partial && h == 0) RED[v * E + e] = G[14 * E + e] * r[0] * r[0];
         if (a.combine >= 0) {
             const double dt = a.dt_is_vector ? a.dt[gid] : a.dt[0];
             double mean = 0.0;
-            double outr[NB];
-            sfor<NB>([&](auto j) {
-                double u0j = 0.0;
-                if (need_u0) {
-                    if constexpr (ORDER <= 2) u0j = u0r[j];
-                    else u0j = a.u0[gid * RS + v * NB + j];
-                }
-                double o;
-                if (a.combine == 1) {
-                    o = 0.5 * ((u0j + c[j]) + dt * r[j]);
-                } else {
-                    o = a.b * (c[j] + dt * r[j]);
-                    if (a.a != 0.0) o = a.a * u0j + o;
-                }
-                outr[j] = o;
-                mean += MEAN_T[j] * o;
+            double outr[NH];
+            hsel(h, [&](auto hc) {
+                sfor<NH>([&](auto j) {
+                    double u0j = 0.0;
+                    if (need_u0) {
+                        if constexpr (ORDER <= 2) u0j = u0r[j];
+                        else u0j = a.u0[gid * RS + v * NB + hc * NH + j];
+                    }
+                    double o;
+                    if (a.combine == 1) {
+                        o = 0.5 * ((u0j + c[j]) + dt * r[j]);
+                    } else {
+                        o = a.b * (c[j] + dt * r[j]);
+                        if (a.a != 0.0) o = a.a * u0j + o;
+                    }
+                    outr[j] = o;
+                    mean += MEAN_T[hc * NH + j] * o;
+                });
             });
-            if constexpr ((NB % 2) == 0) {
+            if constexpr (H == 1 && (NB % 2) == 0) {
 #pragma unroll
                 for (int j = 0; j < NB; j += 2)
                     *reinterpret_cast<double2*>(S + e * RS + v * NB + j) = make_double2(outr[j], outr[j + 1]);
             } else {
 #pragma unroll
-                for (int j = 0; j < NB; ++j) S[e * RS + v * NB + j] = outr[j];
+                for (int j = 0; j < NH; ++j) S[e * RS + v * NB + jb + j] = outr[j];
             }
-            RED[5 * E + v * E + e] = mean;
+            RED[5 * E + h * 5 * E + v * E + e] = mean;
         }
     }
     fence_proxy_async();
     __syncthreads();
     if (t == 0 && a.combine >= 0 && ne > 0) bulk_s2g(a.out + e0 * RS, S, uint32_t(ne) * RS * 8);
-    // epilogues without a trailing barrier: fixed-order shuffle trees
+    // epilogues without a trailing barrier: fixed-order shuffle trees over
+    // the (variable, element) pairs held by threads t < 5E (vn = t / E)
     const int lane = t & 31;
-    if (a.norm_partial) {
+    const int vn = t / E;
+    if (a.norm_partial && t < 5 * E) {
         // partial sum over the tile of vol * res_0^2 per variable; warp w
         // holds variable (32 w) / E (E >= 32) or two variables (E == 16)
         constexpr int W = E < 32 ? E : 32;
-        double x = (live) ? RED[v * E + e] : 0.0;
+        double x = (e < ne) ? RED[vn * E + e] : 0.0;
 #pragma unroll
         for (int o = W / 2; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
         if (E <= 32) {
-            if ((lane % W) == 0) a.norm_partial[int64_t(blockIdx.x) * 5 + v] = x;
+            if ((lane % W) == 0) a.norm_partial[int64_t(blockIdx.x) * 5 + vn] = x;
         } else {  // E == 64: two warps per variable, combined in a fixed order
             __shared__ double half2[10];
             if (lane == 0) half2[(t / 32)] = x;
-            __syncthreads();
+            __syncwarp();
+            asm volatile("bar.sync 1, %0;" ::"r"(5 * E));  // the 5E threads of this epilogue
             if (t < 5) a.norm_partial[int64_t(blockIdx.x) * 5 + t] = half2[2 * t] + half2[2 * t + 1];
         }
     }
-    if (a.combine >= 0 && (a.dt_next || a.dt_vec_out) && v == 0) {
+    if (a.combine >= 0 && (a.dt_next || a.dt_vec_out) && t < E) {
         // CFL dt of the new cell mean (hodg/timestepping.py:121-134), 3D;
-        // threads (0, e) of warp(s) 0 (.. E/32), no other warp waits
+        // threads t < E (element t), no other warp waits
         double dt = 0.0;
         bool okdt = false;
-        if (live) {
-            const double m0 = RED[5 * E + e], m1 = RED[6 * E + e], m2 = RED[7 * E + e], m3 = RED[8 * E + e],
-                         m4 = RED[9 * E + e];
+        if (e < ne) {
+            double mm[5];
+#pragma unroll
+            for (int k = 0; k < 5; ++k) {
+                mm[k] = RED[5 * E + k * E + e];
+#pragma unroll
+                for (int hh = 1; hh < H; ++hh) mm[k] += RED[5 * E + hh * 5 * E + k * E + e];
+            }
+            const double m0 = mm[0], m1 = mm[1], m2 = mm[2], m3 = mm[3], m4 = mm[4];
             if (!(m0 > 0.0)) {
                 flag(err, 2, uint32_t(gid));
             } else {
@@ -663,7 +757,7 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? 4 : 3) elem_stage_k
             unsigned long long bits = okdt ? static_cast<unsigned long long>(__double_as_longlong(dt))
                                            : 0x7FF0000000000000ull;
             constexpr int W = E < 32 ? E : 32;
-            constexpr unsigned mask = E < 32 ? ((1u << E) - 1u) : 0xffffffffu;  // lanes with v == 0
+            constexpr unsigned mask = E < 32 ? ((1u << E) - 1u) : 0xffffffffu;  // lanes t < E
 #pragma unroll
             for (int o = W / 2; o > 0; o >>= 1) {
                 const unsigned long long other = __shfl_xor_sync(mask, bits, o);
@@ -818,7 +912,7 @@ static int launch_face(const hodg_mesh_desc& m, const double* state, void* hbuf,
 template <typename T, bool ES>
 static int launch_elem_k(const hodg_mesh_desc& m, const void* hbuf, const hodg_stage_args& a, uint32_t* err,
                          cudaStream_t st) {
-    const size_t sm = elem_smem_bytes<T>();
+    const size_t sm = elem_smem_bytes<T, ES>();
     static bool attr = false;
     if (!attr) {
         if (cudaFuncSetAttribute(elem_stage_kernel<T, ES>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)) !=
@@ -858,6 +952,7 @@ int HODG_CAT(hodg_launch_elem_p, ORDER)(const hodg_mesh_desc& m, int prec, const
 }
 
 int HODG_CAT(hodg_elem_record_stride_p, ORDER)() { return hodg::HODG_CAT(ord, ORDER)::EREC; }
+int HODG_CAT(hodg_elem_tile_p, ORDER)() { return hodg::HODG_CAT(ord, ORDER)::E; }
 
 int HODG_CAT(hodg_launch_dt_p, ORDER)(const hodg_mesh_desc& m, const double* state, double cfl, double* dt_vec,
                                        unsigned long long* dt_min, uint32_t* err, cudaStream_t st) {

@@ -29,7 +29,32 @@ from .refelem import ref_tables
 
 __all__ = ["GeometryError", "DeviceGeometry", "compute_geometry", "volume_points", "TILE", "tile_major"]
 
-TILE = {0: 64, 1: 64, 2: 32, 3: 16}  # elements per element-kernel CTA (hodg_kernels.cuh: E)
+class _Tiles:
+    """Elements per element-kernel CTA (hodg_kernels.cuh: E), as compiled into
+    libhodg_b200 (hodg_elem_tile); the built-in table if the library is not
+    built yet (host-only use)."""
+
+    _default = {0: 64, 1: 64, 2: 32, 3: 32}
+
+    def __init__(self):
+        self._cache = {}
+
+    def __getitem__(self, order: int) -> int:
+        t = self._cache.get(order)
+        if t is None:
+            try:
+                from . import _lib
+
+                t = int(_lib.load().hodg_elem_tile(int(order)))
+            except Exception:
+                t = self._default[order]
+            if t <= 0:
+                raise KeyError(order)
+            self._cache[order] = t
+        return t
+
+
+TILE = _Tiles()
 
 
 def tile_major(a: np.ndarray, tile: int) -> np.ndarray:

@@ -244,9 +244,10 @@ class Stepper:
     def _records(self, prec):
         """Face flux record buffer: the element-slot layout (one bulk copy per
         element tile, but two record stores per face) or the face-ordered one.
-        "auto" takes the faster per precision on the B200 (profiles/r1k_summary.md):
-        element-slot for mixed precision, face-ordered for FP64."""
-        use_elem = self.layout == "elem" or (self.layout == "auto" and prec == _lib.PREC_MIXED)
+        "auto" takes the faster on the B200: element-slot for
+        mixed precision and at P3, face-ordered for FP64 at P0-P2."""
+        use_elem = self.layout == "elem" or (
+            self.layout == "auto" and (prec == _lib.PREC_MIXED or self.disc.order >= 3))
         return self.disc.elem_buffer(prec) if use_elem else self.disc.face_buffer(prec)
 
     def _stage_args(self, k, parity):
