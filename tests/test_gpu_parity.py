@@ -268,3 +268,31 @@ def test_element_slot_layout_bitwise(P, order, prec):
         got = d.residual_rows(rows, d.face_flux(rows, p, eb), p)
         d.raise_errors()
         assert torch.equal(got, ref), (name, order, prec)
+
+
+@pytest.mark.parametrize("order", [1, 2, 3])
+@pytest.mark.parametrize("prec", [64, 32])
+def test_stepper_layouts_identical_trajectories(P, order, prec):
+    """Fused SSP-RK3 steps (CUDA graphs) with the face-ordered and the
+    element-slot record layouts give bit-identical states and dt."""
+    import torch
+
+    from paper_2209_01877_b200.dg import _get_disc
+    from paper_2209_01877_b200.timestepping import Stepper
+
+    name, m = meshes()[-1]
+    disc_o, c = oracle_state(m, order)
+    gas, geo, bcs = gpu_setup(P, m, order)
+    d = _get_disc(m, geo, gas, bcs)
+    p = P._lib.PREC_F64 if prec == 64 else P._lib.PREC_MIXED
+    out = []
+    for layout in ("face", "elem"):
+        st = Stepper(d, "rk3", p, "global", 0.3, log_norms=True, use_graph=True, layout=layout)
+        st.load(P.DofState(torch.from_numpy(c).cuda()))
+        for _ in range(4):
+            st.step()
+        st.check()
+        out.append((st.state().coeffs.clone(), st.dt_value(), st.norms.clone()))
+    assert torch.equal(out[0][0], out[1][0]), (order, prec)
+    assert out[0][1] == out[1][1]
+    assert torch.equal(out[0][2], out[1][2])
