@@ -245,6 +245,8 @@ def run_ours(args):
     e2e = dofs * n_st * args.steps / e2e_s
     state_bytes = host.numel() * 8
 
+    wc = workload_config(args)
+    assert (wc["elements"], wc["faces"]) == (mesh.n_cells, mesh.n_faces), "Kuhn cube counts"
     peaks, peak_kind = measured_peaks()
     alg = algorithmic_bytes_per_stage(mesh.n_cells, mesh.n_faces, args.order)
     achieved = alg / ((tf + te) * 1e-3) / 1e9
@@ -275,16 +277,12 @@ def run_ours(args):
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
-        "dtype": "f64" if args.prec == 64 else "f32-flux/f64-state",
+        "dtype": dtype_name(args),
         "data": "synthetic Kuhn-cube tetrahedral mesh (random-shuffled then device-RCM renumbered), "
                 "projected isentropic vortex tube",
-        "config": {"workload": f"C1M-class cube n={args.n}: {mesh.n_cells} tets, {mesh.n_faces} faces, "
-                               f"P{args.order} ({NB[args.order]} modes x 5 vars), SSP-RK3, global CFL dt, "
-                               f"{'FP64' if args.prec == 64 else 'mixed FP32-flux/FP64'}",
-                   "elements": mesh.n_cells, "faces": mesh.n_faces, "order": args.order,
-                   "dofs": dofs, "renumbered": not args.no_renumber, "rcm_bandwidth": bw,
-                   "l2": "inputs larger than L2 (state alone is %.0f MB)" % (state_bytes / 1e6),
-                   "parallelism": f"RCB element partition x{world}, NCCL halo" if world > 1 else "single GPU"},
+        "config": dict(workload_config(args), renumbered=not args.no_renumber, rcm_bandwidth=bw,
+                       l2="inputs larger than L2 (state alone is %.0f MB)" % (state_bytes / 1e6),
+                       parallelism=f"RCB element partition x{world}, NCCL halo" if world > 1 else "single GPU"),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
                      "kernel": "RK stage = face_flux_kernel + elem_stage_kernel",
@@ -344,6 +342,20 @@ def cpu_baseline(args):
     return {"value": v, "unit": "DOF-updates/s", "cores": cores, "kind": "port", "sample": sample}
 
 
+def dtype_name(args):
+    return "f64" if args.prec == 64 else "f32-flux/f64-state"
+
+
+def workload_config(args):
+    """The workload both arms name: Kuhn cube of n^3 cells, 6 tets each
+    (N = 6n^3, F = 12n^3 + 6n^2)."""
+    n = args.n
+    ne, nf = 6 * n ** 3, 12 * n ** 3 + 6 * n ** 2
+    return {"workload": f"C1M-class cube n={n}: {ne} tets, {nf} faces, P{args.order} ({NB[args.order]} modes x 5 "
+                        f"vars), SSP-RK3, global CFL dt, {'FP64' if args.prec == 64 else 'mixed FP32-flux/FP64'}",
+            "elements": ne, "faces": nf, "order": args.order, "dofs": ne * 5 * NB[args.order]}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -363,9 +375,9 @@ def run_reference(args):
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
-        "dtype": "f64" if args.prec == 64 else "f32",
+        "dtype": dtype_name(args),
         "data": "synthetic Kuhn-cube tetrahedral mesh, projected isentropic vortex tube",
-        "config": {"workload": f"bounded CPU sample of the C1M P{args.order} SSP-RK3 workload: {sample}"},
+        "config": workload_config(args),
         "cpu_baseline": {"value": v, "unit": "DOF-updates/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": v, "unit": "DOF-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
