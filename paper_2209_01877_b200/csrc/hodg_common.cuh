@@ -107,10 +107,36 @@ struct K {
     static constexpr T one = T(1), half = T(0.5), two = T(2), quarter = T(0.25), efix = T(0.05), zero = T(0);
 };
 
+// Reciprocal and reciprocal square root on the hot paths: in FP64 the MUFU
+// approximation (rcp / rsqrt.approx.ftz.f64, ~2^-22 relative) refined by two
+// Newton steps (quadratic: ~2^-86, i.e. a 1-ulp result) -- no special-case
+// branches and no correctly-rounded division sequence.  Arguments are
+// positive normal numbers on admissible states; an inadmissible state
+// (rho, p or a^2 <= 0) yields garbage that the callers' ok flags discard.
+// FP32 keeps the IEEE operations.
+__device__ __forceinline__ double rcp_nr(double d) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+    double e = fma(-d, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-d, y, 1.0);
+    return fma(y, e, y);
+}
+__device__ __forceinline__ double rsqrt_nr(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double r = fma(-x * y, y, 1.0);
+    y = fma(0.5 * y, r, y);
+    r = fma(-x * y, y, 1.0);
+    return fma(0.5 * y, r, y);
+}
+__device__ __forceinline__ float rcp_nr(float d) { return 1.0f / d; }
+__device__ __forceinline__ float rsqrt_nr(float x) { return rsqrtf(x); }
+
 // primitive (u, v, w, p) from conserved; hodg/physics.py:159-165
 template <typename T>
 __device__ __forceinline__ T prim(const T q[5], T g, T& u, T& v, T& w) {
-    T ri = K<T>::one / q[0];
+    T ri = rcp_nr(q[0]);
     u = q[1] * ri;
     v = q[2] * ri;
     w = q[3] * ri;
@@ -126,7 +152,7 @@ template <typename T>
 __device__ __forceinline__ bool roe(const T qL[5], const T qR[5], const T n[3], T g, T f[5]) {
     const T one = K<T>::one, half = K<T>::half;
     // one rsqrt per side gives both sqrt(rho) and 1/rho
-    const T isL = rsqrt(qL[0]), isR = rsqrt(qR[0]);
+    const T isL = rsqrt_nr(qL[0]), isR = rsqrt_nr(qR[0]);
     const T riL = isL * isL, riR = isR * isR;
     const T sL = qL[0] * isL, sR = qR[0] * isR;
     const T uL = qL[1] * riL, vL = qL[2] * riL, wL = qL[3] * riL;
@@ -137,7 +163,7 @@ __device__ __forceinline__ bool roe(const T qL[5], const T qR[5], const T n[3], 
     const T nx = n[0], ny = n[1], nz = n[2];
     const T vnL = uL * nx + vL * ny + wL * nz;
     const T vnR = uR * nx + vR * ny + wR * nz;
-    const T di = one / (sL + sR);
+    const T di = rcp_nr(sL + sR);
     const T ut = (sL * uL + sR * uR) * di;
     const T vt = (sL * vL + sR * vR) * di;
     const T wt = (sL * wL + sR * wR) * di;
@@ -147,7 +173,7 @@ __device__ __forceinline__ bool roe(const T qL[5], const T qR[5], const T n[3], 
     const T ke = half * (ut * ut + vt * vt + wt * wt);
     const T a2 = gm1 * (Ht - ke);
     const bool ok = (qL[0] > T(0)) & (qR[0] > T(0)) & (pL > T(0)) & (pR > T(0)) & (a2 > T(0));
-    const T ra = rsqrt(a2);
+    const T ra = rsqrt_nr(a2);
     const T a = a2 * ra;
     const T rt = sL * sR;
     const T unt = ut * nx + vt * ny + wt * nz;
