@@ -25,6 +25,13 @@ constexpr int RS = (5 * NB + 1) & ~1;        // state row stride (doubles)
 constexpr int NG = (NQF > 7) ? HODG_NG3 : ((NQF > 1) ? 2 : 1);  // face qp groups per side thread
 constexpr int QPT = (NQF + NG - 1) / NG;     // face qps per phase-1 thread
 constexpr int FACE_THREADS = 128;
+#ifndef HODG_ROE_PAIRS
+#define HODG_ROE_PAIRS 1
+#endif
+#ifndef HODG_FACE_MINB
+#define HODG_FACE_MINB 4
+#endif
+constexpr int RP = HODG_ROE_PAIRS;  // Riemann problems per thread per phase-2 iteration (1 measured fastest)
 constexpr int FT = FACE_THREADS / (2 * NG);  // faces per CTA (32 for P1-P3)
 constexpr int FBS = NQF * NB + 1;            // padded per-slot stride of the smem trace table
 // element kernel: E elements per CTA, thread (v, h, e) -- variable v, basis
@@ -186,7 +193,7 @@ __device__ __forceinline__ void hsel(int h, F&& f) {
 //  record is stored in the blocks of both (owned) neighbours, so the element
 //  kernel fetches a tile's records with one contiguous copy.
 template <typename T, bool BND, bool ES>
-__global__ void __launch_bounds__(FACE_THREADS, 4) face_flux_kernel(const hodg_mesh_desc m,
+__global__ void __launch_bounds__(FACE_THREADS, HODG_FACE_MINB) face_flux_kernel(const hodg_mesh_desc m,
                                                                     const double* __restrict__ state,
                                                                     T* __restrict__ hbuf,
                                                                     uint32_t* __restrict__ err, int64_t f_begin,
@@ -325,14 +332,14 @@ __global__ void __launch_bounds__(FACE_THREADS, 4) face_flux_kernel(const hodg_m
         // phase 2: Riemann flux at each (face, qp); two pairs per thread per
         // iteration so their (straight-line) Roe evaluations interleave
         const int npairs = nf * NQF;
-        for (int p0 = t; p0 < npairs; p0 += 2 * FACE_THREADS) {
-            T qL[2][5], qR[2][5], h[2][5], n[2][3];
-            bool ok[2];
-            int64_t fid[2];
-            int qv[2];
-            int lfv[2];
+        for (int p0 = t; p0 < npairs; p0 += RP * FACE_THREADS) {
+            T qL[RP][5], qR[RP][5], h[RP][5], n[RP][3];
+            bool ok[RP];
+            int64_t fid[RP];
+            int qv[RP];
+            int lfv[RP];
 #pragma unroll
-            for (int k = 0; k < 2; ++k) {
+            for (int k = 0; k < RP; ++k) {
                 const int p = min(p0 + k * FACE_THREADS, npairs - 1);
                 const int lfp = p / NQF;
                 const int q = p - lfp * NQF;
@@ -361,17 +368,17 @@ __global__ void __launch_bounds__(FACE_THREADS, 4) face_flux_kernel(const hodg_m
                 }
             }
             if (m.flux_kind == HODG_FLUX_LLF) {
-#pragma unroll
-                for (int k = 0; k < 2; ++k) ok[k] = ok[k] && llf(qL[k], qR[k], n[k], gam, h[k]);
+                for (int k = 0; k < RP; ++k) ok[k] = ok[k] && llf(qL[k], qR[k], n[k], gam, h[k]);
             } else {
-                const bool r0 = roe(qL[0], qR[0], n[0], gam, h[0]);
-                const bool r1 = roe(qL[1], qR[1], n[1], gam, h[1]);
-                ok[0] = ok[0] && r0;
-                ok[1] = ok[1] && r1;
+                bool r[RP];
+#pragma unroll
+                for (int k = 0; k < RP; ++k) r[k] = roe(qL[k], qR[k], n[k], gam, h[k]);
+#pragma unroll
+                for (int k = 0; k < RP; ++k) ok[k] = ok[k] && r[k];
             }
 #pragma unroll
-            for (int k = 0; k < 2; ++k) {
-                if (k == 1 && p0 + FACE_THREADS >= npairs) break;
+            for (int k = 0; k < RP; ++k) {
+                if (k >= 1 && p0 + k * FACE_THREADS >= npairs) break;
                 if (!ok[k]) {
                     flag(err, 0, uint32_t(fid[k]));
 #pragma unroll
