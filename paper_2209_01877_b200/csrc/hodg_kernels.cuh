@@ -22,7 +22,14 @@ constexpr int RS = (5 * NB + 1) & ~1;        // state row stride (doubles)
 #ifndef HODG_NG3
 #define HODG_NG3 4
 #endif
-constexpr int NG = (NQF > 7) ? HODG_NG3 : ((NQF > 1) ? 2 : 1);  // face qp groups per side thread
+#ifndef HODG_NG2
+#define HODG_NG2 2
+#endif
+#ifndef HODG_NG1
+#define HODG_NG1 2
+#endif
+// face qp groups per side thread (phase 1): bounds the trace accumulators
+constexpr int NG = ORDER == 3 ? HODG_NG3 : (ORDER == 2 ? HODG_NG2 : (ORDER == 1 ? HODG_NG1 : 1));
 constexpr int QPT = (NQF + NG - 1) / NG;     // face qps per phase-1 thread
 constexpr int FACE_THREADS = 128;
 #ifndef HODG_ROE_PAIRS
