@@ -169,6 +169,33 @@ int64_t hodg_rcm_work_bytes(int64_t n, int64_t nnz);
 int hodg_rcm(int64_t n, const int64_t* indptr, const int64_t* indices, int64_t* forward, int64_t* inverse,
              void* work, void* stream);
 
+/* Multi-GPU plumbing (csrc/halo.cu).
+ *
+ * hodg_partition_rcb: host function.  Part id per point by recursive
+ * coordinate bisection of (n, 3) float64 points: split along the first axis
+ * of maximal extent, order by (coordinate, index), the first child takes
+ * (size * floor(k/2)) / k points.  Bit-exact with
+ * paper_2209_01877_b200/partition.py:rcb_partition and oracle/partition.py
+ * (the reference is single-node; METIS-free by design).
+ *
+ * hodg_halo_*: the per-stage ghost-row exchange over NCCL point-to-point.
+ * hodg_halo_unique_id fills a 128-byte ncclUniqueId on one rank (the caller
+ * broadcasts it); hodg_halo_create is collective over the ranks: it builds
+ * the NCCL communicator and uploads the plan -- per peer, the local rows to
+ * send (concatenated in peer order, host or device int32) and the first
+ * local ghost row / count to receive.  hodg_halo_exchange packs the send
+ * rows (one kernel) and posts the grouped sends and receives on `stream`;
+ * ghost rows land directly in `state` ((rows, rs) float64, device).  NCCL is
+ * taken from the process's libnccl.so.2 at run time. */
+int hodg_partition_rcb(int64_t n, const double* points, int nparts, int32_t* part);
+typedef struct hodg_halo hodg_halo;
+int hodg_halo_unique_id(void* id128);
+int hodg_halo_create(int nranks, int rank, const void* id128, int npeers, const int32_t* peers,
+                     const int64_t* send_count, const int32_t* send_rows, const int64_t* recv_first,
+                     const int64_t* recv_count, int rs, hodg_halo** out);
+int hodg_halo_exchange(hodg_halo* halo, double* state, void* stream);
+int hodg_halo_destroy(hodg_halo* halo);
+
 /* 2D table-driven path: the reference's own discretisation (triangles and
  * bilinear quads, 4 variables, per-cell quadrature tables of
  * hodg/geometry.py:120-220) with the argument lists of the reference kernels

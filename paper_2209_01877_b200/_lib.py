@@ -81,6 +81,11 @@ SIGNATURES = {
     "hodg_elem_stage_es": (I32, [P, I32, P, C.POINTER(StageArgs), P, P]),
     "hodg_elem_record_stride": (I32, [I32]),
     "hodg_elem_record_len": (I64, [P, I32]),
+    "hodg_partition_rcb": (I32, [I64, P, I32, P]),
+    "hodg_halo_unique_id": (I32, [P]),
+    "hodg_halo_create": (I32, [I32, I32, P, I32, P, P, P, P, P, I32, C.POINTER(C.c_void_p)]),
+    "hodg_halo_exchange": (I32, [P, P, P]),
+    "hodg_halo_destroy": (I32, [P]),
     "hodg_local_dt": (I32, [P, P, D, P, P, P, P]),
     "hodg_norm_finalize": (I32, [P, I64, P, P]),
     "hodg_residual_l2": (I32, [P, P, P, P, P]),

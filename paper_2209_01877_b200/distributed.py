@@ -22,7 +22,7 @@ from . import _lib
 from .dg import BoundaryConditions, Discretization, DofState
 from .geometry import compute_geometry
 from .mesh import TetMesh
-from .partition import HaloExchange, LocalPart, build_local, rcb_partition
+from .partition import HaloExchange, LocalPart, NativeHaloExchange, build_local, rcb_partition
 from .physics import GasModel
 from .timestepping import SCHEMES, Stepper
 
@@ -30,12 +30,32 @@ __all__ = ["DistributedStepper", "setup_partitioned"]
 
 
 class DistributedStepper(Stepper):
+    """halo: "native" -- the library's NCCL exchange (`hodg_halo_*`, its own
+    communicator, unique id broadcast over `group`); "torch" -- point-to-point
+    ops of the torch.distributed group (the gloo CPU tests); "auto" -- native
+    on CUDA devices (override with HODG_HALO=torch)."""
+
     def __init__(self, part: LocalPart, disc: Discretization, scheme="rk3", prec=_lib.PREC_F64, cfl=0.3,
-                 log_norms=True, group=None):
+                 log_norms=True, group=None, halo="auto"):
+        import os
+
+        import torch
+        import torch.distributed as dist
+
         super().__init__(disc, scheme, prec, "global", cfl, log_norms=log_norms, use_graph=False)
         self.part = part
         self.group = group
-        self.halo = HaloExchange(part, disc.device, group)
+        if halo == "auto":
+            halo = os.environ.get("HODG_HALO", "native" if torch.device(disc.device).type == "cuda" else "torch")
+        if halo == "native":
+            rank, world = dist.get_rank(group), dist.get_world_size(group)
+            uid = [NativeHaloExchange.unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0, group=group)
+            self.halo = NativeHaloExchange(part, disc.rs, rank, world, uid[0], disc.device)
+        elif halo == "torch":
+            self.halo = HaloExchange(part, disc.device, group)
+        else:
+            raise ValueError(f"unknown halo exchange {halo!r}")
         self.norm_sums = None
 
     def _allreduce_dt(self, slot_index):

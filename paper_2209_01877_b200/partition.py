@@ -25,32 +25,24 @@ import numpy as np
 
 from .mesh import BoundaryPatch, TetMesh
 
-__all__ = ["rcb_partition", "LocalPart", "build_local", "HaloExchange"]
+__all__ = ["rcb_partition", "LocalPart", "build_local", "HaloExchange", "NativeHaloExchange"]
 
 
 def rcb_partition(points: np.ndarray, nparts: int) -> np.ndarray:
-    """Part id per point (int32) by recursive coordinate bisection."""
-    pts = np.asarray(points, dtype=np.float64)
+    """Part id per point (int32) by recursive coordinate bisection: the
+    library's `hodg_partition_rcb` (host C++, csrc/halo.cu)."""
+    from . import _lib
+
+    pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
     n = pts.shape[0]
     if nparts < 1:
         raise ValueError("nparts must be >= 1")
     if nparts > max(n, 1):
         raise ValueError("more parts than elements")
     parts = np.zeros(n, dtype=np.int32)
-    stack = [(np.arange(n, dtype=np.int64), 0, nparts)]
-    while stack:
-        ids, base, k = stack.pop()
-        if k == 1:
-            parts[ids] = base
-            continue
-        sub = pts[ids]
-        ext = sub.max(axis=0) - sub.min(axis=0)
-        axis = int(np.argmax(ext))  # first maximal axis
-        order = ids[np.lexsort((ids, sub[:, axis]))]
-        k1 = k // 2
-        n1 = (ids.size * k1) // k
-        stack.append((order[n1:], base + k1, k - k1))
-        stack.append((order[:n1], base, k1))
+    if n:
+        _lib.check(_lib.load().hodg_partition_rcb(n, pts.ctypes.data, int(nparts), parts.ctypes.data),
+                   "hodg_partition_rcb")
     return parts
 
 
@@ -174,3 +166,79 @@ class HaloExchange:
         for w in self._work:
             w.wait()
         self._work = []
+
+
+class NativeHaloExchange:
+    """The same exchange through the library's NCCL halo (`hodg_halo_*`,
+    csrc/halo.cu): one pack kernel plus grouped NCCL sends / receives on a
+    communication stream, ghost rows received in place.  `start` orders the
+    exchange after the work already queued on the current stream (the state
+    rows are ready); `wait` makes the current stream wait for it, so the
+    interior-face kernel runs while the halo is in flight.
+
+    `nranks == 1` with the rank as its own peer is the single-GPU self test
+    (tests/test_gpu_halo.py)."""
+
+    def __init__(self, part: LocalPart, rs: int, rank: int, nranks: int, unique_id: bytes, device="cuda"):
+        import ctypes as C
+
+        import torch
+
+        from . import _lib
+
+        self.L = _lib.lib()
+        self.part = part
+        peers = sorted(set(part.send_idx) | set(part.recv_range))
+        send_count = [len(part.send_idx.get(q, ())) for q in peers]
+        rows = np.concatenate([np.asarray(part.send_idx[q], dtype=np.int32) for q in peers if q in part.send_idx]) \
+            if part.send_idx else np.zeros(1, dtype=np.int32)
+        recv_first = [part.recv_range.get(q, (0, 0))[0] for q in peers]
+        recv_count = [part.recv_range.get(q, (0, 0))[1] for q in peers]
+        arr = lambda v, t: np.ascontiguousarray(np.asarray(v, dtype=t))  # noqa: E731
+        self._keep = (arr(peers, np.int32), arr(send_count, np.int64), arr(rows, np.int32),
+                      arr(recv_first, np.int64), arr(recv_count, np.int64))
+        uid = C.create_string_buffer(bytes(unique_id), 128)
+        h = C.c_void_p()
+        k = self._keep
+        _lib.check(self.L.hodg_halo_create(int(nranks), int(rank), uid, len(peers), k[0].ctypes.data,
+                                           k[1].ctypes.data, k[2].ctypes.data, k[3].ctypes.data, k[4].ctypes.data,
+                                           int(rs), C.byref(h)), "hodg_halo_create")
+        self.handle = h
+        self.stream = torch.cuda.Stream(device=device)
+        self._ready = torch.cuda.Event()
+        self._done = torch.cuda.Event()
+
+    @staticmethod
+    def unique_id() -> bytes:
+        import ctypes as C
+
+        from . import _lib
+
+        buf = C.create_string_buffer(128)
+        _lib.check(_lib.lib().hodg_halo_unique_id(buf), "hodg_halo_unique_id")
+        return buf.raw
+
+    def start(self, rows):
+        from . import _lib
+
+        self._ready.record()
+        self.stream.wait_event(self._ready)
+        _lib.check(self.L.hodg_halo_exchange(self.handle, _lib.ptr(rows), _lib.stream_ptr(self.stream)),
+                   "hodg_halo_exchange")
+        self._done.record(self.stream)
+
+    def wait(self):
+        import torch
+
+        torch.cuda.current_stream().wait_event(self._done)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.L.hodg_halo_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
