@@ -194,6 +194,10 @@ int hodg_halo_create(int nranks, int rank, const void* id128, int npeers, const 
                      const int64_t* send_count, const int32_t* send_rows, const int64_t* recv_first,
                      const int64_t* recv_count, int rs, hodg_halo** out);
 int hodg_halo_exchange(hodg_halo* halo, double* state, void* stream);
+/* in-place all-reduce on the halo's communicator (stream-ordered, so a
+ * distributed step captures into one CUDA graph): kind 0 = int64 MIN (the dt
+ * slot, positive doubles as bit patterns: exact), kind 1 = float64 SUM. */
+int hodg_halo_allreduce(hodg_halo* halo, void* buf, int64_t count, int kind, void* stream);
 int hodg_halo_destroy(hodg_halo* halo);
 
 /* 2D table-driven path: the reference's own discretisation (triangles and

@@ -85,6 +85,7 @@ SIGNATURES = {
     "hodg_halo_unique_id": (I32, [P]),
     "hodg_halo_create": (I32, [I32, I32, P, I32, P, P, P, P, P, I32, C.POINTER(C.c_void_p)]),
     "hodg_halo_exchange": (I32, [P, P, P]),
+    "hodg_halo_allreduce": (I32, [P, P, I64, I32, P]),
     "hodg_halo_destroy": (I32, [P]),
     "hodg_local_dt": (I32, [P, P, D, P, P, P, P]),
     "hodg_norm_finalize": (I32, [P, I64, P, P]),

@@ -77,6 +77,8 @@ struct Nccl {
     ncclResult_t (*GroupEnd)() = nullptr;
     ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
     bool ok = false;
 };
 
@@ -95,7 +97,9 @@ const Nccl& nccl() {
     n.GroupEnd = reinterpret_cast<decltype(n.GroupEnd)>(dlsym(h, "ncclGroupEnd"));
     n.Send = reinterpret_cast<decltype(n.Send)>(dlsym(h, "ncclSend"));
     n.Recv = reinterpret_cast<decltype(n.Recv)>(dlsym(h, "ncclRecv"));
-    n.ok = n.GetUniqueId && n.CommInitRank && n.CommDestroy && n.GroupStart && n.GroupEnd && n.Send && n.Recv;
+    n.AllReduce = reinterpret_cast<decltype(n.AllReduce)>(dlsym(h, "ncclAllReduce"));
+    n.ok = n.GetUniqueId && n.CommInitRank && n.CommDestroy && n.GroupStart && n.GroupEnd && n.Send && n.Recv &&
+           n.AllReduce;
     return n;
 }
 
@@ -220,6 +224,17 @@ int hodg_halo_exchange(hodg_halo* h, double* state, void* stream) {
             return HODG_ECUDA;
     }
     return n.GroupEnd() == ncclSuccess ? HODG_OK : HODG_ECUDA;
+}
+
+int hodg_halo_allreduce(hodg_halo* h, void* buf, int64_t count, int kind, void* stream) {
+    if (!h || !buf || count < 0 || kind < 0 || kind > 1) return HODG_EINVAL;
+    const Nccl& n = nccl();
+    // kind 0: int64 MIN (dt slots as double bit patterns: exact); 1: float64 SUM
+    const ncclDataType_t t = kind == 0 ? ncclInt64 : ncclFloat64;
+    const ncclRedOp_t op = kind == 0 ? ncclMin : ncclSum;
+    return n.AllReduce(buf, buf, size_t(count), t, op, h->comm, static_cast<cudaStream_t>(stream)) == ncclSuccess
+               ? HODG_OK
+               : HODG_ECUDA;
 }
 
 int hodg_halo_destroy(hodg_halo* h) {

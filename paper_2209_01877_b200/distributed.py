@@ -42,11 +42,16 @@ class DistributedStepper(Stepper):
         import torch
         import torch.distributed as dist
 
+        if halo == "auto":
+            halo = os.environ.get("HODG_HALO", "native" if torch.device(disc.device).type == "cuda" else "torch")
+        # eager launches: the exchange and the reductions are stream-ordered
+        # (no host sync per step), so the host runs ahead of the GPU; NCCL
+        # point-to-point inside CUDA-graph capture is not used (a captured
+        # self-exchange hung on the B200 test box)
         super().__init__(disc, scheme, prec, "global", cfl, log_norms=log_norms, use_graph=False)
         self.part = part
         self.group = group
-        if halo == "auto":
-            halo = os.environ.get("HODG_HALO", "native" if torch.device(disc.device).type == "cuda" else "torch")
+        self.native = halo == "native"
         if halo == "native":
             rank, world = dist.get_rank(group), dist.get_world_size(group)
             uid = [NativeHaloExchange.unique_id() if rank == 0 else None]
@@ -63,11 +68,20 @@ class DistributedStepper(Stepper):
 
         s = self.slots[slot_index:slot_index + 1]
         # positive doubles order like their int64 bit patterns: MIN is exact
-        dist.all_reduce(s, op=dist.ReduceOp.MIN, group=self.group)
+        if self.native:
+            self.halo.allreduce(s, 0)
+        else:
+            dist.all_reduce(s, op=dist.ReduceOp.MIN, group=self.group)
 
     def init_dt(self):
         super().init_dt()
         self._allreduce_dt(self.parity)
+
+    def warm(self):
+        """First launches outside graph capture on a halo-complete state."""
+        self.halo.start(self.A)
+        self.halo.wait()
+        super().warm()
 
     def _launch_step(self, parity):
         import torch
@@ -90,7 +104,10 @@ class DistributedStepper(Stepper):
         if self.log_norms:
             import torch.distributed as dist
 
-            dist.all_reduce(self.norm_sums, op=dist.ReduceOp.SUM, group=self.group)
+            if self.native:
+                self.halo.allreduce(self.norm_sums, 1)
+            else:
+                dist.all_reduce(self.norm_sums, op=dist.ReduceOp.SUM, group=self.group)
             self.norms.copy_(torch.sqrt(self.norm_sums))
 
     def launches_per_step(self) -> int:

@@ -232,6 +232,13 @@ class NativeHaloExchange:
 
         torch.cuda.current_stream().wait_event(self._done)
 
+    def allreduce(self, t, kind):
+        """In place on the current stream: kind 0 int64 MIN, 1 float64 SUM."""
+        from . import _lib
+
+        _lib.check(self.L.hodg_halo_allreduce(self.handle, _lib.ptr(t), t.numel(), int(kind), _lib.stream_ptr()),
+                   "hodg_halo_allreduce")
+
     def close(self):
         if getattr(self, "handle", None):
             self.L.hodg_halo_destroy(self.handle)

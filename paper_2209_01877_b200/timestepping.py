@@ -213,6 +213,7 @@ class Stepper:
         self.steps = 0
         self._graphs = {}
         self._args = []
+        self.capture_mode = "global"
 
     # -- state in / out ----------------------------------------------------
     def load(self, state: DofState):
@@ -312,7 +313,7 @@ class Stepper:
                 s = torch.cuda.Stream()
                 s.wait_stream(torch.cuda.current_stream())
                 g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g, stream=s):
+                with torch.cuda.graph(g, stream=s, capture_error_mode=self.capture_mode):
                     self._launch_step(p)
                 torch.cuda.current_stream().wait_stream(s)
                 self._graphs[p] = g

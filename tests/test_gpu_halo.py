@@ -147,3 +147,4 @@ def test_distributed_stepper_native_halo_single_rank(P):
         ds.halo.close()
     finally:
         dist.destroy_process_group()
+
