@@ -111,7 +111,8 @@ def build_case(n, order, renumber, device):
 
     mesh = P.generate_tet_box(n, extent=(0.0, 0.0, 0.0, 10.0, 10.0, 10.0),
                               bc={"xmin": "far_field", "xmax": "far_field", "ymin": "far_field",
-                                  "ymax": "far_field", "zmin": "slip_wall", "zmax": "slip_wall"})
+                                  "ymax": "far_field", "zmin": "slip_wall", "zmax": "slip_wall"},
+                              device=device)  # connectivity + geometry on the GPU (bit-identical)
     bw = None
     if renumber:
         # shuffled input (randomize_cells = 1), then device RCM + face re-sort

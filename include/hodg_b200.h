@@ -50,6 +50,7 @@ extern "C" {
 #define HODG_EINVAL 2
 #define HODG_ECUDA 3
 #define HODG_ENODEV 4
+#define HODG_ETOPOLOGY 5 /* hodg_mesh_setup: non-manifold face / zero-area face / degenerate element */
 
 /* boundary kinds, hodg/physics.py:47-50 */
 #define HODG_BC_INTERIOR 0
@@ -168,6 +169,25 @@ int hodg_err_decode(const uint32_t* err_host, int64_t* id);
 int64_t hodg_rcm_work_bytes(int64_t n, int64_t nnz);
 int hodg_rcm(int64_t n, const int64_t* indptr, const int64_t* indices, int64_t* forward, int64_t* inverse,
              void* work, void* stream);
+
+/* Device mesh setup (csrc/setup.cu): connectivity
+ * by sorted face keys and the per-face / per-element geometry of
+ * paper_2209_01877_b200/mesh.py:build_tet_mesh on the GPU, same numbering
+ * (face id = rank of its first traversal, element-major slot order; the
+ * first traverser is the left element; slot f is the face opposite sorted
+ * vertex f).  Inputs (device): X (n_nodes, 3) float64, tets (n_elems, 4)
+ * int32 with each row ascending.  Outputs (device, sized for the upper bound
+ * F <= 4 n_elems): face_cells (F,2), face_slots (F,2) int8, face_nodes (F,3),
+ * face_normal (F,3), face_area (F,), cell_faces / cell_fsign /
+ * cell_neighbors (n,4), cell_volume (n,), cell_centroid (n,3), cell_h (n,);
+ * *n_faces_out = F.  Synchronous (reads F back).  HODG_ETOPOLOGY with
+ * *n_faces_out = -1 non-manifold, -2 zero-area face, -3 degenerate element.
+ * Limits: n_nodes < 2^21 (64-bit packed key), 4 n_elems < 2^31. */
+int64_t hodg_mesh_setup_work_bytes(int64_t n_elems);
+int hodg_mesh_setup(int64_t n_nodes, int64_t n_elems, const double* X, const int32_t* tets, int32_t* face_cells,
+                    int8_t* face_slots, int32_t* face_nodes, double* face_normal, double* face_area,
+                    int32_t* cell_faces, int8_t* cell_fsign, int32_t* cell_neighbors, double* cell_volume,
+                    double* cell_centroid, double* cell_h, int64_t* n_faces_out, void* work, void* stream);
 
 /* Multi-GPU plumbing (csrc/halo.cu).
  *

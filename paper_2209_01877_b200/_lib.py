@@ -82,6 +82,8 @@ SIGNATURES = {
     "hodg_elem_record_stride": (I32, [I32]),
     "hodg_elem_record_len": (I64, [P, I32]),
     "hodg_partition_rcb": (I32, [I64, P, I32, P]),
+    "hodg_mesh_setup_work_bytes": (I64, [I64]),
+    "hodg_mesh_setup": (I32, [I64, I64] + [P] * 16),
     "hodg_halo_unique_id": (I32, [P]),
     "hodg_halo_create": (I32, [I32, I32, P, I32, P, P, P, P, P, I32, C.POINTER(C.c_void_p)]),
     "hodg_halo_exchange": (I32, [P, P, P]),

@@ -128,9 +128,12 @@ def _signed_volume6(V):
     return np.einsum("nd,nd->n", a, np.cross(b, c))
 
 
-def build_tet_mesh(node_xyz, tets, patch_specs=None) -> TetMesh:
+def build_tet_mesh(node_xyz, tets, patch_specs=None, device=None) -> TetMesh:
     """Assemble a tetrahedral mesh from nodes, element->node lists and
-    boundary patches [(name, kind, [(a, b, c), ...]), ...]."""
+    boundary patches [(name, kind, [(a, b, c), ...]), ...].  With `device`
+    (e.g. "cuda") the connectivity and geometry are built on the GPU
+    (`hodg_mesh_setup`, csrc/setup.cu): identical integer arrays, float
+    geometry equal up to libm-vs-CUDA rounding of the element size h."""
     X = np.ascontiguousarray(node_xyz, dtype=np.float64)
     if X.ndim != 2 or X.shape[1] != 3:
         raise MeshError("node coordinates must be an (n, 3) array")
@@ -145,6 +148,13 @@ def build_tet_mesh(node_xyz, tets, patch_specs=None) -> TetMesh:
     if np.any(T[:, 1:] == T[:, :-1]):
         raise TopologyError("element with a repeated node")
     n = T.shape[0]
+    nn = np.int64(X.shape[0])
+    if device is not None:
+        (face_cells, face_slots, face_nodes, normal, area, cell_faces, cell_fsign, cell_neighbors, vol, centroid,
+         h) = _setup_on_device(X, T, device)
+        F = face_cells.shape[0]
+        return _with_patches(X, T, patch_specs, nn, F, face_nodes, face_cells, cell_faces, cell_fsign,
+                             cell_neighbors, centroid, vol, h, face_slots, normal, area)
     V = X[T]
     vol = np.abs(_signed_volume6(V)) / 6.0
     if np.any(vol <= 0.0):
@@ -153,7 +163,6 @@ def build_tet_mesh(node_xyz, tets, patch_specs=None) -> TetMesh:
     h = np.cbrt(vol)
 
     # face discovery: pack the ascending triple into one 64-bit key
-    nn = np.int64(X.shape[0])
     tri = T[:, FACE_LOCAL].reshape(-1, 3)  # (4n, 3), slot-major within element
     key = (tri[:, 0] * nn + tri[:, 1]) * nn + tri[:, 2]
     order = np.argsort(key, kind="stable")  # ties keep traversal order
@@ -199,7 +208,44 @@ def build_tet_mesh(node_xyz, tets, patch_specs=None) -> TetMesh:
 
     fc = face_cells[cell_faces]
     cell_neighbors = np.where(fc[..., 0] == np.arange(n)[:, None], fc[..., 1], fc[..., 0]).astype(np.int32)
+    return _with_patches(X, T, patch_specs, nn, F, face_nodes, face_cells, cell_faces, cell_fsign, cell_neighbors,
+                         centroid, vol, h, face_slots, normal, area)
 
+
+def _setup_on_device(X, T, device):
+    """hodg_mesh_setup: connectivity + geometry on the GPU, copied back."""
+    import torch
+
+    from . import _lib
+
+    L = _lib.lib()
+    n = T.shape[0]
+    dev = torch.device(device)
+    up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    Xd, Td = up(X), up(T.astype(np.int32))
+    cap = 4 * n
+    e = lambda shape, dt: torch.empty(shape, dtype=dt, device=dev)  # noqa: E731
+    out = [e((cap, 2), torch.int32), e((cap, 2), torch.int8), e((cap, 3), torch.int32), e((cap, 3), torch.float64),
+           e(cap, torch.float64), e((n, 4), torch.int32), e((n, 4), torch.int8), e((n, 4), torch.int32),
+           e(n, torch.float64), e((n, 3), torch.float64), e(n, torch.float64)]
+    wb = int(L.hodg_mesh_setup_work_bytes(n))
+    if wb < 0:
+        raise MeshError("mesh too large for the device setup")
+    work = e(wb, torch.uint8)
+    nf = np.zeros(1, dtype=np.int64)
+    rc = L.hodg_mesh_setup(X.shape[0], n, _lib.ptr(Xd), _lib.ptr(Td), *[_lib.ptr(t) for t in out], nf.ctypes.data,
+                           _lib.ptr(work), _lib.stream_ptr())
+    if rc == 5:  # HODG_ETOPOLOGY
+        raise TopologyError({-1: "face shared by more than two elements (non-manifold)", -2: "zero-area face",
+                             -3: "degenerate element (zero volume)"}.get(int(nf[0]), "invalid topology"))
+    _lib.check(rc, "hodg_mesh_setup")
+    F = int(nf[0])
+    fc, fs, fn, nrm, area, cf, cs, cn, vol, cen, h = [t.cpu().numpy() for t in out]
+    return fc[:F], fs[:F], fn[:F], nrm[:F], area[:F], cf, cs, cn, vol, cen, h
+
+
+def _with_patches(X, T, patch_specs, nn, F, face_nodes, face_cells, cell_faces, cell_fsign, cell_neighbors,
+                  centroid, vol, h, face_slots, normal, area) -> TetMesh:
     face_patch = np.full(F, -1, dtype=np.int32)
     patches = []
     if patch_specs:
@@ -230,7 +276,7 @@ _SIDES = ("xmin", "xmax", "ymin", "ymax", "zmin", "zmax")
 
 
 def generate_tet_box(nx: int, ny: int | None = None, nz: int | None = None,
-                     extent=(0.0, 0.0, 0.0, 1.0, 1.0, 1.0), bc="far_field") -> TetMesh:
+                     extent=(0.0, 0.0, 0.0, 1.0, 1.0, 1.0), bc="far_field", device=None) -> TetMesh:
     """Structured hexahedral lattice, each hex split into six tetrahedra
     along its main diagonal (conforming; 6 nx ny nz elements).  `bc` is one
     kind or a dict keyed by xmin..zmax.  Elements are numbered hex-major
@@ -275,7 +321,7 @@ def generate_tet_box(nx: int, ny: int | None = None, nz: int | None = None,
         lo, hi = corner(0, 0), corner(1, 1)
         tris = np.concatenate([np.stack([lo, corner(1, 0), hi], axis=1), np.stack([lo, corner(0, 1), hi], axis=1)])
         specs.append((side, kinds[side], tris))
-    return build_tet_mesh(nodes, elems.reshape(-1, 4), specs)
+    return build_tet_mesh(nodes, elems.reshape(-1, 4), specs, device=device)
 
 
 def perturb_interior_nodes(mesh: TetMesh, amplitude: float, seed: int = 0) -> TetMesh:
