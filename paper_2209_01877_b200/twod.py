@@ -26,6 +26,7 @@ from .precision import PrecisionController, PrecisionSchedule
 from .quadrature import gauss_legendre_1d, triangle_rule
 
 __all__ = ["Mesh2D", "build_mesh_2d", "generate_quad_grid", "generate_tri_grid", "perturb_interior_nodes",
+           "save_mesh_2d", "load_mesh_2d",
            "compute_geometry_2d", "Device2D", "RunConfig2D", "run2d", "residual_csv_text"]
 
 BC_KINDS = ("far_field", "slip_wall", "no_slip_wall")
@@ -179,6 +180,128 @@ def perturb_interior_nodes(m: Mesh2D, amplitude, seed=0) -> Mesh2D:
     cells = [tuple(m.cell_nodes[c, : m.cell_nvert[c]]) for c in range(m.n_cells)]
     specs = [(p.name, p.kind, [tuple(m.face_nodes[f]) for f in p.face_ids]) for p in m.patches]
     return build_mesh_2d(xy, cells, specs)
+
+
+# ---------------------------------------------------------------------------
+# HODG-MESH v1 (hodg/mesh.py:431-560): the reference's 2D plain-text format
+
+
+def save_mesh_2d(m: Mesh2D, path) -> None:
+    """hodg/mesh.py:431-447 (byte-identical output)."""
+    with open(path, "w") as fh:
+        fh.write("hodg-mesh 1\n")
+        fh.write(f"nodes {m.node_xy.shape[0]}\n")
+        for x, y in m.node_xy:
+            fh.write(f"{float(x)!r} {float(y)!r}\n")
+        fh.write(f"cells {m.n_cells}\n")
+        for c in range(m.n_cells):
+            nv = int(m.cell_nvert[c])
+            fh.write(("t" if nv == 3 else "q") + " " + " ".join(str(int(v)) for v in m.cell_nodes[c, :nv]) + "\n")
+        fh.write(f"patches {len(m.patches)}\n")
+        for p in m.patches:
+            fh.write(f"{p.name} {p.kind} {len(p.face_ids)}\n")
+            for f in p.face_ids:
+                a, b = m.face_nodes[f]
+                fh.write(f"{int(a)} {int(b)}\n")
+
+
+def load_mesh_2d(path) -> Mesh2D:
+    """hodg/mesh.py:450-560: MeshParseError with the line number on malformed
+    input, TopologyError on bad connectivity."""
+    from .mesh import MeshParseError, TopologyError
+
+    with open(path) as fh:
+        lines = fh.read().splitlines()
+    pos = 0
+
+    def next_line():
+        nonlocal pos
+        while pos < len(lines):
+            raw = lines[pos]
+            pos += 1
+            t = raw.strip()
+            if t and not t.startswith("#"):
+                return pos, t
+        return pos, None
+
+    def err(ln, msg):
+        return MeshParseError(path, ln, msg)
+
+    def count(tag):
+        ln, t = next_line()
+        if t is None or not t.startswith(tag + " "):
+            raise err(ln, f"expected '{tag} N'")
+        try:
+            return int(t.split()[1])
+        except (IndexError, ValueError):
+            raise err(ln, f"bad {tag} count") from None
+
+    ln, t = next_line()
+    if t is None or t.split() != ["hodg-mesh", "1"]:
+        raise err(ln, "expected header 'hodg-mesh 1'")
+    nn = count("nodes")
+    xy = np.empty((nn, 2))
+    for i in range(nn):
+        ln, t = next_line()
+        if t is None:
+            raise err(ln, f"expected {nn} node lines, got {i}")
+        parts = t.split()
+        if len(parts) != 2:
+            raise err(ln, "expected 'x y'")
+        try:
+            xy[i] = (float(parts[0]), float(parts[1]))
+        except ValueError:
+            raise err(ln, f"bad coordinate {t!r}") from None
+    nc = count("cells")
+    cells = []
+    for i in range(nc):
+        ln, t = next_line()
+        if t is None:
+            raise err(ln, f"expected {nc} cell lines, got {i}")
+        parts = t.split()
+        want = {"t": 3, "q": 4}.get(parts[0])
+        if want is None or len(parts) != want + 1:
+            raise err(ln, "expected 't i j k' or 'q i j k l'")
+        try:
+            cells.append(tuple(int(v) for v in parts[1:]))
+        except ValueError:
+            raise err(ln, f"bad node index in {t!r}") from None
+    specs = []
+    ln, t = next_line()
+    if t is not None:
+        if not t.startswith("patches "):
+            raise err(ln, "expected 'patches P'")
+        try:
+            npatch = int(t.split()[1])
+        except (IndexError, ValueError):
+            raise err(ln, "bad patch count") from None
+        for _ in range(npatch):
+            ln, t = next_line()
+            parts = t.split() if t is not None else []
+            if len(parts) != 3:
+                raise err(ln, "expected 'name kind count'")
+            name, kind = parts[0], parts[1]
+            if kind not in BC_KINDS:
+                raise err(ln, f"unknown boundary kind {kind!r}")
+            try:
+                cnt = int(parts[2])
+            except ValueError:
+                raise err(ln, "bad face count") from None
+            pairs = []
+            for _ in range(cnt):
+                ln, t = next_line()
+                parts = t.split() if t is not None else []
+                if len(parts) != 2:
+                    raise err(ln, "expected 'nodeA nodeB'")
+                try:
+                    pairs.append((int(parts[0]), int(parts[1])))
+                except ValueError:
+                    raise err(ln, f"bad node index in {t!r}") from None
+            specs.append((name, kind, pairs))
+    try:
+        return build_mesh_2d(xy, cells, specs)
+    except (ValueError, KeyError) as e:
+        raise TopologyError(f"{path}: {e}") from None
 
 
 # ---------------------------------------------------------------------------
@@ -533,6 +656,7 @@ class Device2D:
 class RunConfig2D:
     """The reference RunConfig fields its fixture runs use (hodg/config.py:28-75)."""
 
+    mesh_path: str | None = None  # HODG-MESH v1 file instead of the generator
     gen_kind: str = "quad"
     gen_nx: int = 16
     gen_ny: int = 16
@@ -588,8 +712,11 @@ def run2d(cfg: RunConfig2D):
     """hodg/timestepping.py:256-357 with the passes on the GPU."""
     import torch
 
-    gen = generate_quad_grid if cfg.gen_kind == "quad" else generate_tri_grid
-    m = gen(cfg.gen_nx, cfg.gen_ny, cfg.gen_extent, cfg.gen_bc)
+    if cfg.mesh_path is not None:
+        m = load_mesh_2d(cfg.mesh_path)
+    else:
+        gen = generate_quad_grid if cfg.gen_kind == "quad" else generate_tri_grid
+        m = gen(cfg.gen_nx, cfg.gen_ny, cfg.gen_extent, cfg.gen_bc)
     t = compute_geometry_2d(m, cfg.order)
     prim_inf, qinf = freestream_2d(cfg.gamma, cfg.R, cfg.mach, cfg.angle_deg)
     x = t.vol_xy[:, :, 0].ravel()

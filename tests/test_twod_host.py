@@ -42,3 +42,29 @@ def test_mu_from_reynolds_and_pulse_field():
     ref = S.pulse_primitive(S.Gas(), 0.2, 0.3, 0.0, 0.0, x, 0 * x, 0.4, 10.0)
     for a, b in zip((rho, u, v, p), ref):
         assert np.array_equal(a, b)
+
+
+def test_hodg_mesh_v1_roundtrip_with_reference_files(tmp_path):
+    """load_mesh_2d reads the reference's own save_mesh output
+    (tests/golden/mesh_*.hodg) into the same mesh the generators build, and
+    save_mesh_2d writes it back byte for byte (hodg/mesh.py:431-560)."""
+    from conftest import golden_path
+    from paper_2209_01877_b200.mesh import MeshParseError
+
+    gens = {"quad_perturbed": lambda: twod.perturb_interior_nodes(twod.generate_quad_grid(6, 5), 0.15, seed=3),
+            "tri_perturbed": lambda: twod.perturb_interior_nodes(twod.generate_tri_grid(5, 4), 0.12, seed=7)}
+    for name, gen in gens.items():
+        path = golden_path(f"mesh_{name}.hodg")
+        m = twod.load_mesh_2d(path)
+        g = gen()
+        for f in ("node_xy", "cell_nodes", "cell_faces", "cell_fsign", "face_nodes", "face_cells", "face_normal",
+                  "face_length", "face_patch"):
+            assert np.array_equal(getattr(m, f), getattr(g, f)), (name, f)
+        out = tmp_path / f"{name}.hodg"
+        twod.save_mesh_2d(m, out)
+        assert out.read_bytes() == open(path, "rb").read()
+    bad = tmp_path / "bad.hodg"
+    bad.write_text("hodg-mesh 1\nnodes 2\n0 0\n1 x\n")
+    with pytest.raises(MeshParseError) as e:
+        twod.load_mesh_2d(bad)
+    assert e.value.line_no == 4

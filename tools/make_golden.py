@@ -20,6 +20,8 @@ reference package `hodg` (numba) and writes:
                                        corpus: aux gradient, qhat, finv, fvis,
                                        fqhat and the residual, orders 0-2, at
                                        float64 and float32
+  mesh_quad_perturbed.hodg,            reference save_mesh output (HODG-MESH v1)
+  mesh_tri_perturbed.hodg              of two corpus meshes
   residuals_ns_dp.csv,                 reference Navier-Stokes runs: a viscous
   residuals_ns_mp.csv                  vortex (order 2) and a small version of
                                        the c07 pulse case (mp_fixed switch)
@@ -114,6 +116,11 @@ def main():
             st32 = dg.DofState(st.coeffs.astype(np.float32))
             arrays[f"{name}_p{order}_res32"] = dg.rhs(st32, m, geo, bcs, gas).res
     np.savez_compressed(os.path.join(OUT, "ref_rhs2d.npz"), **arrays)
+
+    # HODG-MESH v1 files written by the reference
+    for name, m in corpus():
+        if name in ("quad_perturbed", "tri_perturbed"):
+            M.save_mesh(m, os.path.join(OUT, f"mesh_{name}.hodg"))
 
     # viscous passes (pkg/tests/test_dg.py:12, mu = 0.02)
     ns = GasModel(mu_dyn=0.02, ivis=1)
