@@ -296,3 +296,57 @@ def test_stepper_layouts_identical_trajectories(P, order, prec):
     assert torch.equal(out[0][0], out[1][0]), (order, prec)
     assert out[0][1] == out[1][1]
     assert torch.equal(out[0][2], out[1][2])
+
+
+_C_BC = {"xmin": "far_field", "xmax": "far_field", "ymin": "far_field", "ymax": "far_field",
+         "zmin": "slip_wall", "zmax": "slip_wall"}
+
+
+def test_config0_against_fixture(P):
+    """BASELINE config 0 on the GPU against the committed oracle fixture
+    (tests/golden/config0_*, tools/make_golden_3d.py): residual history per
+    entry and final state within 1e-12."""
+    from conftest import golden_path
+
+    m = P.perturb_interior_nodes(P.generate_tet_box(4, extent=(0.0, 0.0, 0.0, 10.0, 10.0, 2.5), bc=_C_BC), 0.1, 3)
+    cfg = P.RunConfig(order=1, mach=0.5, initial_kind="vortex", initial_x0=5.0, initial_y0=5.0, cfl=0.3,
+                      dt_mode="global", scheme="rk3", max_iterations=10, log_every=1)
+    art = P.run(cfg, mesh=m)
+    rows = [r.split(",") for r in open(golden_path("config0_residuals.csv")).read().strip().splitlines()[1:]]
+    ref = np.array([[float(x) for x in r[1:7]] for r in rows])
+    got = np.column_stack([np.array(art.history.res), np.array(art.history.dts)])
+    assert np.max(np.abs(got - ref) / np.abs(ref)) <= FP64_TOL
+    u = np.load(golden_path("config0_state.npz"))["coeffs"]
+    assert rel(art.final_state.coeffs.cpu().numpy(), u) <= FP64_TOL
+
+
+@pytest.mark.parametrize("prec", [64, 32])
+def test_c200k_against_oracle(P, prec):
+    """BASELINE config 1 at its full size (C200k: Kuhn cube n = 32, 196,608
+    tets, P2): freestream preserved to 1e-11, and three SSP-RK3 steps of the
+    vortex agree with the oracle (16 host threads) -- FP64 1e-12, mixed 1e-5
+    on the state."""
+    import torch
+
+    m = P.generate_tet_box(32, extent=(0.0, 0.0, 0.0, 10.0, 10.0, 10.0), bc=_C_BC, device="cuda")
+    assert m.n_cells == 196608
+    gas = P.GasModel()
+    geo = P.compute_geometry(m, 2)
+    bcs = P.BoundaryConditions(P.freestream_conserved(gas, 0.5, 0.0))
+    fs = P.project_initial(m, geo, lambda x, y, z: P.freestream_primitive(gas, 0.5, 0.0), gas)
+    if prec == 64:
+        r = P.rhs(fs, m, geo, bcs, gas).res
+        assert float(r.abs().max()) < 1e-11
+    om = to_oracle(m)
+    spec = S.RunSpec(mesh=om, order=2, mach=0.5, initial="vortex", x0=5.0, y0=5.0, cfl=0.3, dt_mode="global",
+                     scheme="rk3", max_iterations=3, log_every=1, precision_mode="dp")
+    u_ref, hist, _ = S.run(spec)
+    cfg = P.RunConfig(order=2, mach=0.5, initial_kind="vortex", initial_x0=5.0, initial_y0=5.0, cfl=0.3,
+                      dt_mode="global", scheme="rk3", max_iterations=3, log_every=1,
+                      precision_mode="dp" if prec == 64 else "sp")
+    art = P.run(cfg, mesh=m)
+    got = art.final_state.coeffs.double().cpu().numpy()
+    tol = FP64_TOL if prec == 64 else MIXED_TOL
+    assert rel(got, u_ref) <= tol, rel(got, u_ref)
+    if prec == 64:
+        assert rel(np.array(art.history.res), np.array(hist.res)) <= tol
