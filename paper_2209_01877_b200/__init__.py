@@ -9,7 +9,7 @@ local_dt_field, min_reduce, run, rcm, apply_permutation, ...).
 """
 
 from .mesh import (BC_KINDS, BoundaryPatch, MeshError, MeshParseError, TetMesh, TopologyError, build_tet_mesh,
-                   generate_tet_box, load_mesh, perturb_interior_nodes, save_mesh, validate)
+                   generate_tet_box, generate_wing_box, load_mesh, perturb_interior_nodes, save_mesh, validate)
 from .physics import (AdmissibilityError, Conserved, GasModel, Primitive, freestream_conserved,
                       freestream_primitive, vortex_primitive)
 from .geometry import DeviceGeometry, compute_geometry

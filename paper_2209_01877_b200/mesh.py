@@ -324,6 +324,65 @@ def generate_tet_box(nx: int, ny: int | None = None, nz: int | None = None,
     return build_tet_mesh(nodes, elems.reshape(-1, 4), specs, device=device)
 
 
+def generate_wing_box(n: int, sweep_deg: float = 30.0, span: float = 0.6, root_chord: float = 0.35,
+                      taper: float = 0.56, thickness: float = 0.10, device=None) -> TetMesh:
+    """BASELINE config 4's synthetic ONERA-M6-like geometry:
+    the Kuhn-split unit cube of n^3 hexahedra with a swept, tapered
+    diamond-section wedge wing cut out -- hexahedra whose centre lies inside
+    the wing are removed (a lattice-conforming, staircase surface).  The wing
+    root sits on the z = 0 symmetry plane (slip wall), its leading edge at
+    x = 0.3 + z tan(sweep), chord root_chord (1 - (1 - taper) z / span),
+    half-thickness `thickness` x chord x min(xi / 0.3, (1 - xi) / 0.7) about
+    y = 0.5.  Boundaries: wing surface `wing` (slip wall), z = 0 `symmetry`
+    (slip wall), the other five sides far field."""
+    if n < 4:
+        raise MeshError("wing box needs n >= 4")
+    g = np.linspace(0.0, 1.0, n + 1)
+    nodes = np.stack(np.meshgrid(g, g, g, indexing="ij"), axis=-1).transpose(2, 1, 0, 3).reshape(-1, 3)
+
+    def nid(i, j, k):
+        return (k * (n + 1) + j) * (n + 1) + i
+
+    k3, j3, i3 = np.meshgrid(np.arange(n), np.arange(n), np.arange(n), indexing="ij")
+    i3, j3, k3 = i3.ravel(), j3.ravel(), k3.ravel()
+    xc, yc, zc = (i3 + 0.5) / n, (j3 + 0.5) / n, (k3 + 0.5) / n
+    chord = root_chord * (1.0 - (1.0 - taper) * zc / span)
+    xi = (xc - (0.3 + zc * np.tan(np.deg2rad(sweep_deg)))) / chord
+    half = thickness * chord * np.minimum(xi / 0.3, (1.0 - xi) / 0.7)
+    inside = (zc <= span) & (xi >= 0.0) & (xi <= 1.0) & (np.abs(yc - 0.5) <= half)
+    keep = ~inside
+    i3, j3, k3 = i3[keep], j3[keep], k3[keep]
+    elems = np.empty((i3.size, 6, 4), dtype=np.int64)
+    for p, path in enumerate(_PATHS):
+        off = np.zeros(3, dtype=np.int64)
+        elems[:, p, 0] = nid(i3, j3, k3)
+        for s_, ax in enumerate(path):
+            off[ax] += 1
+            elems[:, p, s_ + 1] = nid(i3 + off[0], j3 + off[1], k3 + off[2])
+    # unreferenced nodes (strictly inside the wing) are dropped
+    used = np.unique(elems)
+    remap = np.full(nodes.shape[0], -1, dtype=np.int64)
+    remap[used] = np.arange(used.size)
+    m = build_tet_mesh(nodes[used], remap[elems.reshape(-1, 4)], None, device=device)
+    bnd = np.flatnonzero(m.face_cells[:, 1] < 0)
+    X = m.node_xy[m.face_nodes[bnd].astype(np.int64)]
+    eps = 1e-12
+    on = lambda d, v: np.all(np.abs(X[:, :, d] - v) < eps, axis=1)  # noqa: E731
+    sym = on(2, 0.0)
+    outer = on(0, 0.0) | on(0, 1.0) | on(1, 0.0) | on(1, 1.0) | on(2, 1.0)
+    wing = ~(sym | outer)
+    face_patch = np.full(m.n_faces, -1, dtype=np.int32)
+    patches = []
+    for p, (name, kind, sel) in enumerate((("far", "far_field", outer), ("symmetry", "slip_wall", sym),
+                                            ("wing", "slip_wall", wing))):
+        ids = np.sort(bnd[sel]).astype(np.int32)
+        face_patch[ids] = p
+        patches.append(BoundaryPatch(name, kind, ids))
+    return TetMesh(m.node_xy, m.cell_nodes, m.cell_faces, m.cell_fsign, m.cell_neighbors, m.cell_centroid,
+                   m.cell_area, m.cell_h, m.face_nodes, m.face_cells, m.face_slots, m.face_normal, m.face_length,
+                   face_patch, patches)
+
+
 def perturb_interior_nodes(mesh: TetMesh, amplitude: float, seed: int = 0) -> TetMesh:
     """Interior nodes moved by amplitude x (shortest incident edge) x
     U(-1, 1)^3; boundary nodes fixed, patches preserved (3D analogue of

@@ -350,3 +350,24 @@ def test_c200k_against_oracle(P, prec):
     assert rel(got, u_ref) <= tol, rel(got, u_ref)
     if prec == 64:
         assert rel(np.array(art.history.res), np.array(hist.res)) <= tol
+
+
+def test_wing_against_oracle(P):
+    """BASELINE config 4's wedge-wing geometry (generate_wing_box; slip walls
+    on the wing and the symmetry plane): watertight, and two SSP-RK3 steps of
+    the incident freestream (P1, FP64) match the oracle to 1e-12."""
+    m = P.generate_wing_box(12, thickness=0.3, device="cuda")
+    bnd = m.face_cells[:, 1] < 0
+    closure = (m.face_normal[bnd] * m.face_length[bnd][:, None]).sum(axis=0)
+    assert np.abs(closure).max() < 1e-13
+    assert {p.name: p.kind for p in m.patches} == {"far": "far_field", "symmetry": "slip_wall",
+                                                    "wing": "slip_wall"}
+    assert m.patches[2].face_ids.size > 0
+    cfg = P.RunConfig(order=1, mach=0.5, angle_deg=3.0, initial_kind="freestream", cfl=0.3, dt_mode="global",
+                      scheme="rk3", max_iterations=2, log_every=1)
+    art = P.run(cfg, mesh=m)
+    spec = S.RunSpec(mesh=to_oracle(m), order=1, mach=0.5, angle_deg=3.0, initial="freestream", cfl=0.3,
+                     dt_mode="global", scheme="rk3", max_iterations=2, log_every=1)
+    u, hist, _ = S.run(spec)
+    assert rel(art.final_state.coeffs.cpu().numpy(), u) <= FP64_TOL
+    assert rel(np.array(art.history.res), np.array(hist.res)) <= FP64_TOL
