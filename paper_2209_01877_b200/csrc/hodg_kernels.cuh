@@ -58,7 +58,11 @@ constexpr int E = (ORDER >= 3) ? (H > 1 ? 32 : 16) : (ORDER == 2 ? HODG_E2 : 64)
 constexpr int NH = NB / H;
 static_assert(NB % H == 0 && (H == 1 || E >= 32) && 5 * H <= 15, "basis split layout");
 constexpr int ETHREADS = 5 * E * H;
-constexpr int EMINB = H > 1 ? 2 : 3;  // CTAs per SM the FP64 element kernel is register-budgeted for
+constexpr int EMINB = H > 1 ? 2 : 3;
+#ifndef HODG_U0_TMA_ORDER
+#define HODG_U0_TMA_ORDER 0  // orders >= this fetch u0 by TMA after the volume phases (else: registers)
+#endif
+constexpr bool U0_TMA = ORDER >= HODG_U0_TMA_ORDER;  // CTAs per SM the FP64 element kernel is register-budgeted for
 constexpr int XS = 15;                        // smem slot per (element, qp): 5 traces -> 15 contravariant fluxes
 #ifndef HODG_QC2
 #define HODG_QC2 7
@@ -493,7 +497,7 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : 4) : E
     const bool need_u0 = a.combine == 1 || (a.combine == 0 && a.a != 0.0);
     const int jb = h * NH;  // first basis function of this thread's part
     double c[NH];
-    double u0r[(ORDER <= 2) ? NH : 1];
+    double u0r[!U0_TMA ? NH : 1];
     if (live) {
         if constexpr (H == 1 && (NB % 2) == 0) {
             ld_row(S + e * RS + v * NB, c);  // rows 16-byte aligned when NB is even
@@ -501,7 +505,7 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : 4) : E
 #pragma unroll
             for (int i = 0; i < NH; ++i) c[i] = S[e * RS + v * NB + jb + i];
         }
-        if constexpr (ORDER <= 2) {
+        if constexpr (!U0_TMA) {
             if (need_u0) {
                 if constexpr (H == 1 && (NB % 2) == 0) {
                     ld_row(a.u0 + gid * RS + v * NB, u0r);
@@ -614,6 +618,18 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : 4) : E
         __syncthreads();
     });
 
+    // P3: the u0 tile is not held in registers through the volume phases;
+    // one TMA copy into the freed state / X region, in flight during the
+    // gather and the solve (each thread later reads, then overwrites with
+    // its output, only its own entries)
+    if constexpr (U0_TMA) {
+        if (need_u0 && t == 0 && ne > 0) {
+            const uint32_t bs = uint32_t(ne) * RS * 8;
+            fence_proxy_async();
+            mbar_arrive_expect_tx(bar, bs);
+            bulk_g2s(S, a.u0 + e0 * RS, bs, bar);
+        }
+    }
     // face gather, mass solve, RK update
     mbar_wait(bar + 1, 0);
     double accd[NH];
@@ -681,6 +697,9 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : 4) : E
         }
         if (a.norm_partial && h == 0) RED[v * E + e] = G[14 * E + e] * r[0] * r[0];
         if (a.combine >= 0) {
+            if constexpr (U0_TMA) {
+                if (need_u0) mbar_wait(bar, 1);
+            }
             const double dt = a.dt_is_vector ? a.dt[gid] : a.dt[0];
             double mean = 0.0;
             double outr[NH];
@@ -688,8 +707,8 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : 4) : E
                 sfor<NH>([&](auto j) {
                     double u0j = 0.0;
                     if (need_u0) {
-                        if constexpr (ORDER <= 2) u0j = u0r[j];
-                        else u0j = a.u0[gid * RS + v * NB + hc * NH + j];
+                        if constexpr (!U0_TMA) u0j = u0r[j];
+                        else u0j = S[e * RS + v * NB + hc * NH + j];  // u0 tile (TMA, above)
                     }
                     double o;
                     if (a.combine == 1) {
