@@ -58,7 +58,11 @@ constexpr int E = (ORDER >= 3) ? (H > 1 ? 32 : 16) : (ORDER == 2 ? HODG_E2 : 64)
 constexpr int NH = NB / H;
 static_assert(NB % H == 0 && (H == 1 || E >= 32) && 5 * H <= 15, "basis split layout");
 constexpr int ETHREADS = 5 * E * H;
-constexpr int EMINB = H > 1 ? 2 : 3;
+#ifndef HODG_EMINB
+#define HODG_EMINB 0
+#endif
+// CTAs per SM the FP64 element kernel is register-budgeted for
+constexpr int EMINB = HODG_EMINB ? HODG_EMINB : (H > 1 ? 2 : 3);
 #ifndef HODG_U0_TMA_ORDER
 #define HODG_U0_TMA_ORDER 0  // orders >= this fetch u0 by TMA after the volume phases (else: registers)
 #endif
