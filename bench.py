@@ -151,6 +151,7 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dist_mode = world > 1 or args.partitioned
     if dist_mode:
+        os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29511")
         dist.init_process_group("nccl", init_method="env://", rank=rank, world_size=world)
@@ -321,6 +322,8 @@ def run_ours(args):
         line["cpu_baseline"] = cpu_baseline(args)
         print(json.dumps(line), flush=True)
     if dist_mode:
+        torch.cuda.synchronize()
+        st.close()  # the library's NCCL communicator before the process group
         dist.destroy_process_group()
 
 

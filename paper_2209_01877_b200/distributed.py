@@ -113,6 +113,13 @@ class DistributedStepper(Stepper):
     def launches_per_step(self) -> int:
         return 3 * len(SCHEMES[self.scheme])
 
+    def close(self):
+        """Release the exchange (the native one owns an NCCL communicator);
+        call before destroying the process group."""
+        close = getattr(self.halo, "close", None)
+        if close is not None:
+            close()
+
     def gather_state(self):
         """Global (n_cells, 5, nb) Taylor coefficients on every rank."""
         import torch
