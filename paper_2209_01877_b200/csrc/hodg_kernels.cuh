@@ -54,7 +54,10 @@ constexpr int H = (ORDER == 3) ? HODG_H3 : (ORDER == 2 ? HODG_H2 : 1);
 #ifndef HODG_E2
 #define HODG_E2 32
 #endif
-constexpr int E = (ORDER >= 3) ? (H > 1 ? 32 : 16) : (ORDER == 2 ? HODG_E2 : 64);  // elements per CTA
+#ifndef HODG_E1
+#define HODG_E1 32
+#endif
+constexpr int E = (ORDER >= 3) ? (H > 1 ? 32 : 16) : (ORDER == 2 ? HODG_E2 : (ORDER == 1 ? HODG_E1 : 64));
 constexpr int NH = NB / H;
 static_assert(NB % H == 0 && (H == 1 || E >= 32) && 5 * H <= 15, "basis split layout");
 constexpr int ETHREADS = 5 * E * H;

@@ -34,7 +34,7 @@ class _Tiles:
     libhodg_b200 (hodg_elem_tile); the built-in table if the library is not
     built yet (host-only use)."""
 
-    _default = {0: 64, 1: 64, 2: 32, 3: 32}
+    _default = {0: 64, 1: 32, 2: 32, 3: 32}
 
     def __init__(self):
         self._cache = {}
