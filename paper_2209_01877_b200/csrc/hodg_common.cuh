@@ -107,6 +107,9 @@ struct K {
     static constexpr T one = T(1), half = T(0.5), two = T(2), quarter = T(0.25), efix = T(0.05), zero = T(0);
 };
 
+#ifndef HODG_F32_FAST_RCP
+#define HODG_F32_FAST_RCP 1
+#endif
 // Reciprocal and reciprocal square root on the hot paths: in FP64 the MUFU
 // approximation (rcp / rsqrt.approx.ftz.f64, ~2^-22 relative) refined by two
 // Newton steps (quadratic: ~2^-86, i.e. a 1-ulp result) -- no special-case
@@ -130,7 +133,15 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
     r = fma(-x * y, y, 1.0);
     return fma(0.5 * y, r, y);
 }
-__device__ __forceinline__ float rcp_nr(float d) { return 1.0f / d; }
+__device__ __forceinline__ float rcp_nr(float d) {
+#if HODG_F32_FAST_RCP
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(d));
+    return fmaf(y, fmaf(-d, y, 1.0f), y);  // one Newton step: ~1 ulp
+#else
+    return 1.0f / d;
+#endif
+}
 __device__ __forceinline__ float rsqrt_nr(float x) { return rsqrtf(x); }
 
 // primitive (u, v, w, p) from conserved; hodg/physics.py:159-165
