@@ -52,3 +52,37 @@ def test_host_side_argument_checks():
     assert L.hodg_err_decode(err, C.byref(idv)) == 2 and idv.value == 12
     ok = (C.c_uint32 * 4)(0xFFFFFFFF, 0xFFFFFFFF, 0xFFFFFFFF, 0xFFFFFFFF)
     assert L.hodg_err_decode(ok, C.byref(idv)) == 0
+
+
+def test_host_side_edge_cases():
+    """Invalid or empty inputs are rejected before any device work (the
+    reference's argument-validation tests, restated for the ABI)."""
+    import numpy as np
+
+    from paper_2209_01877_b200 import _lib
+
+    L = _lib.load()
+    EINVAL = _lib.HODG_EINVAL
+    # element-slot record strides: 20 NQF + 1 (odd)
+    strides = [L.hodg_elem_record_stride(p) for p in range(4)]
+    assert strides == [21, 121, 141, 301] and all(s % 2 == 1 for s in strides)
+    assert L.hodg_elem_record_stride(4) == -1 and L.hodg_elem_record_stride(-1) == -1
+    assert L.hodg_face_record_stride(2, 16) == -1
+    # device mesh setup sizing
+    assert L.hodg_mesh_setup_work_bytes(0) == -1 and L.hodg_mesh_setup_work_bytes(1 << 29) == -1
+    assert L.hodg_mesh_setup_work_bytes(1000) > 0
+    # RCB: bounds and determinism on host
+    pts = np.random.default_rng(0).random((10, 3))
+    part = np.zeros(10, dtype=np.int32)
+    assert L.hodg_partition_rcb(10, pts.ctypes.data, 11, part.ctypes.data) == EINVAL
+    assert L.hodg_partition_rcb(0, pts.ctypes.data, 1, part.ctypes.data) == EINVAL
+    assert L.hodg_partition_rcb(10, pts.ctypes.data, 0, part.ctypes.data) == EINVAL
+    assert L.hodg_partition_rcb(10, pts.ctypes.data, 10, part.ctypes.data) == _lib.HODG_OK
+    assert sorted(part.tolist()) == list(range(10))
+    # null handles / buffers
+    assert L.hodg_face_flux(None, 64, None, None, None, None) == EINVAL
+    assert L.hodg_elem_stage(None, 64, None, None, None, None) == EINVAL
+    assert L.hodg_halo_exchange(None, None, None) == EINVAL
+    assert L.hodg_halo_destroy(None) == _lib.HODG_OK
+    assert L.hodg2d_qhat_pass(64, 0, 2, 3, *([None] * 8), 1.4, None, None, None) == EINVAL
+    assert L.hodg2d_aux_pass(64, 5, 7, 4, 2, 4, *([None] * 17)) == EINVAL  # nb > 6
