@@ -61,6 +61,9 @@ constexpr int E = (ORDER >= 3) ? (H > 1 ? 32 : 16) : (ORDER == 2 ? HODG_E2 : (OR
 constexpr int NH = NB / H;
 static_assert(NB % H == 0 && (H == 1 || E >= 32) && 5 * H <= 15, "basis split layout");
 constexpr int ETHREADS = 5 * E * H;
+#ifndef HODG_PDL
+#define HODG_PDL 0  // element kernel launched as a programmatic dependent of the face kernel
+#endif
 #ifndef HODG_EMINB
 #define HODG_EMINB 0
 #endif
@@ -293,6 +296,7 @@ __global__ void __launch_bounds__(FACE_THREADS, HODG_FACE_MINB) face_flux_kernel
         }
     };
 
+    if constexpr (HODG_PDL) asm volatile("griddepcontrol.launch_dependents;");
     int tile = blockIdx.x;
     Meta cur = load_meta(tile);
     __syncthreads();  // barrier init visible
@@ -471,6 +475,8 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : 4) : E
             mbar_arrive_expect_tx(bar, bs + 16 * E * 8);
             bulk_g2s(S, a.us + e0 * RS, bs, bar);
             bulk_g2s(G, m.egeo + tile * 16 * E, 16 * E * 8, bar);
+            // the records are the face kernel's output
+            if constexpr (HODG_PDL) asm volatile("griddepcontrol.wait;" ::: "memory");
             mbar_arrive_expect_tx(bar + 1, hb);
             bulk_g2s(HT, hbuf + e0 * EREC, hb, bar + 1);
         } else {
@@ -482,6 +488,9 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : 4) : E
     }
     __syncthreads();
     mbar_wait(bar, 0);
+    // programmatic dependent launch: everything above overlapped the face
+    // kernel's tail; records, and the in-place output, need it complete
+    if constexpr (HODG_PDL) asm volatile("griddepcontrol.wait;" ::: "memory");
 
     // thread (v, h, e): e fastest, so h is warp-uniform (E >= 32 when H > 1)
     const int e = t % E;
@@ -961,8 +970,26 @@ static int launch_elem_k(const hodg_mesh_desc& m, const void* hbuf, const hodg_s
         attr = true;
     }
     const int64_t nblk = (m.n_elems + E - 1) / E;
-    if (nblk > 0)
-        elem_stage_kernel<T, ES><<<unsigned(nblk), ETHREADS, sm, st>>>(m, static_cast<const T*>(hbuf), a, err);
+    if (nblk > 0) {
+        if constexpr (HODG_PDL) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(unsigned(nblk));
+            cfg.blockDim = dim3(ETHREADS);
+            cfg.dynamicSmemBytes = sm;
+            cfg.stream = st;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            if (cudaLaunchKernelEx(&cfg, elem_stage_kernel<T, ES>, m, static_cast<const T*>(hbuf), a, err) !=
+                cudaSuccess)
+                return HODG_ECUDA;
+        } else {
+            elem_stage_kernel<T, ES>
+                <<<unsigned(nblk), ETHREADS, sm, st>>>(m, static_cast<const T*>(hbuf), a, err);
+        }
+    }
     return cudaGetLastError() == cudaSuccess ? HODG_OK : HODG_ECUDA;
 }
 
