@@ -26,7 +26,7 @@ from .precision import PrecisionController, PrecisionSchedule
 from .quadrature import gauss_legendre_1d, triangle_rule
 
 __all__ = ["Mesh2D", "build_mesh_2d", "generate_quad_grid", "generate_tri_grid", "perturb_interior_nodes",
-           "save_mesh_2d", "load_mesh_2d",
+           "save_mesh_2d", "load_mesh_2d", "write_vtk_2d",
            "compute_geometry_2d", "Device2D", "RunConfig2D", "run2d", "residual_csv_text"]
 
 BC_KINDS = ("far_field", "slip_wall", "no_slip_wall")
@@ -302,6 +302,42 @@ def load_mesh_2d(path) -> Mesh2D:
         return build_mesh_2d(xy, cells, specs)
     except (ValueError, KeyError) as e:
         raise TopologyError(f"{path}: {e}") from None
+
+
+def write_vtk_2d(path, m: Mesh2D, t: "Tables2D", coeffs, gamma: float = 1.4) -> None:
+    """Cell-mean flow field (rho, u, v, p, Mach) of a state -- a device
+    tensor or an array -- on the unstructured grid, in the reference's
+    legacy-VTK layout (hodg/output.py:54-83; byte-identical for the same
+    state).  The means are the reference's einsum (hodg/dg.py:666-668)."""
+    if hasattr(coeffs, "detach"):
+        coeffs = coeffs.detach().cpu().numpy()
+    means = np.einsum("cvj,cj->cv", np.asarray(coeffs).astype(np.float64), t.basis_mean)
+    rho = means[:, 0]
+    u = means[:, 1] / rho
+    v = means[:, 2] / rho
+    p = (gamma - 1.0) * (means[:, 3] - 0.5 * rho * (u * u + v * v))
+    a = np.sqrt(np.maximum(gamma * p / rho, 0.0))
+    mach = np.divide(np.hypot(u, v), a, out=np.zeros_like(a), where=a > 0)
+    with open(path, "w") as fh:
+        fh.write("# vtk DataFile Version 3.0\n")
+        fh.write("hodg cell-mean flow field\n")
+        fh.write("ASCII\nDATASET UNSTRUCTURED_GRID\n")
+        fh.write(f"POINTS {m.node_xy.shape[0]} double\n")
+        for x, y in m.node_xy:
+            fh.write(f"{float(x)!r} {float(y)!r} 0.0\n")
+        sizes = m.cell_nvert.astype(np.int64)
+        fh.write(f"CELLS {m.n_cells} {int(np.sum(sizes + 1))}\n")
+        for c in range(m.n_cells):
+            nv = int(sizes[c])
+            fh.write(f"{nv} " + " ".join(str(int(n)) for n in m.cell_nodes[c, :nv]) + "\n")
+        fh.write(f"CELL_TYPES {m.n_cells}\n")
+        for c in range(m.n_cells):
+            fh.write("5\n" if sizes[c] == 3 else "9\n")
+        fh.write(f"CELL_DATA {m.n_cells}\n")
+        for name, vals in (("rho", rho), ("u", u), ("v", v), ("p", p), ("Mach", mach)):
+            fh.write(f"SCALARS {name} double 1\nLOOKUP_TABLE default\n")
+            for val in vals:
+                fh.write(f"{float(val)!r}\n")
 
 
 # ---------------------------------------------------------------------------

@@ -68,3 +68,17 @@ def test_hodg_mesh_v1_roundtrip_with_reference_files(tmp_path):
     with pytest.raises(MeshParseError) as e:
         twod.load_mesh_2d(bad)
     assert e.value.line_no == 4
+
+
+def test_vtk_field_matches_reference_file(tmp_path):
+    """write_vtk_2d writes the reference's legacy-VTK cell-mean field byte
+    for byte (hodg/output.py:54-83; tests/golden/field_tri_perturbed_p2.vtk
+    from tools/make_golden.py)."""
+    from conftest import golden_path
+
+    m = twod.perturb_interior_nodes(twod.generate_tri_grid(5, 4), 0.12, seed=7)
+    t = twod.compute_geometry_2d(m, 2)
+    c = np.load(golden_path("ref_rhs2d.npz"))["tri_perturbed_p2_coeffs"]
+    out = tmp_path / "f.vtk"
+    twod.write_vtk_2d(out, m, t, c, 1.4)
+    assert out.read_bytes() == open(golden_path("field_tri_perturbed_p2.vtk"), "rb").read()

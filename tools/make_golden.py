@@ -20,6 +20,7 @@ reference package `hodg` (numba) and writes:
                                        corpus: aux gradient, qhat, finv, fvis,
                                        fqhat and the residual, orders 0-2, at
                                        float64 and float32
+  field_tri_perturbed_p2.vtk           reference write_vtk of a corpus state
   mesh_quad_perturbed.hodg,            reference save_mesh output (HODG-MESH v1)
   mesh_tri_perturbed.hodg              of two corpus meshes
   residuals_ns_dp.csv,                 reference Navier-Stokes runs: a viscous
@@ -117,10 +118,17 @@ def main():
             arrays[f"{name}_p{order}_res32"] = dg.rhs(st32, m, geo, bcs, gas).res
     np.savez_compressed(os.path.join(OUT, "ref_rhs2d.npz"), **arrays)
 
-    # HODG-MESH v1 files written by the reference
+    # HODG-MESH v1 files written by the reference, and a VTK field of a
+    # corpus state (hodg/output.py:54-83)
+    from hodg.output import write_vtk
+
     for name, m in corpus():
         if name in ("quad_perturbed", "tri_perturbed"):
             M.save_mesh(m, os.path.join(OUT, f"mesh_{name}.hodg"))
+        if name == "tri_perturbed":
+            geo = compute_geometry(m, 2)
+            st = dg.DofState(np.load(os.path.join(OUT, "ref_rhs2d.npz"))[f"{name}_p2_coeffs"])
+            write_vtk(os.path.join(OUT, "field_tri_perturbed_p2.vtk"), m, st, geo, gas)
 
     # viscous passes (pkg/tests/test_dg.py:12, mu = 0.02)
     ns = GasModel(mu_dyn=0.02, ivis=1)
