@@ -77,14 +77,6 @@ __device__ __forceinline__ void bulk_wait_read() {
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
-// Ampere-style 16-byte async copies (LDGSTS): the gather of scattered
-// rows (element states per face, face records per element), where one TMA
-// bulk copy per row would be issued serially by the warp
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // make generic-proxy smem writes visible to the async (TMA) proxy
 __device__ __forceinline__ void fence_proxy_async() {
