@@ -236,22 +236,27 @@ def run_ours(args):
     out_host = torch.empty_like(host).pin_memory()
     norms = torch.empty(5, dtype=torch.float64).pin_memory()
     errh = torch.empty(4, dtype=torch.int32).pin_memory()
-    barrier()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    dev_state = P.DofState(host.to("cuda", non_blocking=True))
-    st.load(dev_state)
-    for _ in range(args.steps):
-        # (distributed: every rank reads its norms / error word each step)
-        st.step()
-        norms.copy_(st.norms, non_blocking=True)
-        errh.copy_(disc.err, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-        if np.any(errh.numpy().astype(np.uint32) != 0xFFFFFFFF) or not np.all(np.isfinite(norms.numpy())):
-            raise RuntimeError("solver error during e2e run")
-    out_host.copy_(st.state().coeffs, non_blocking=True)
-    torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t0
+
+    def e2e_pass():
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        dev_state = P.DofState(host.to("cuda", non_blocking=True))
+        st.load(dev_state)
+        for _ in range(args.steps):
+            # (distributed: every rank reads its norms / error word each step)
+            st.step()
+            norms.copy_(st.norms, non_blocking=True)
+            errh.copy_(disc.err, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            if np.any(errh.numpy().astype(np.uint32) != 0xFFFFFFFF) or not np.all(np.isfinite(norms.numpy())):
+                raise RuntimeError("solver error during e2e run")
+        out_host.copy_(st.state().coeffs, non_blocking=True)
+        torch.cuda.synchronize()
+        return time.perf_counter() - t0
+
+    e2e_pass()  # untimed warm-up pass (the caching allocator's first 400 MB blocks)
+    e2e_s = e2e_pass()
     if world > 1:
         t = torch.tensor([e2e_s], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

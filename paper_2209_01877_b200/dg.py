@@ -194,8 +194,11 @@ class Discretization:
         c = torch.as_tensor(coeffs, device=self.device).to(torch.float64)
         if tuple(c.shape) != (self.n, N_VARS, self.nb):
             raise ValueError(f"state shape {tuple(c.shape)} != {(self.n, N_VARS, self.nb)}")
-        src = self.new_state()
-        src[: self.n, : N_VARS * self.nb] = c.reshape(self.n, -1)
+        if self.rs == N_VARS * self.nb and self.n_rows == self.n and c.is_contiguous():
+            src = c  # the (5, nb) blocks already are the kernel's rows: no staging copy
+        else:
+            src = self.new_state()
+            src[: self.n, : N_VARS * self.nb] = c.reshape(self.n, -1)
         out = self.new_state() if out is None else out
         _lib.check(self.L.hodg_modal_transform(self.handle, 1, _lib.ptr(src), _lib.ptr(out), _lib.stream_ptr()),
                    "hodg_modal_transform")
@@ -206,7 +209,8 @@ class Discretization:
         out = self.new_state()
         _lib.check(self.L.hodg_modal_transform(self.handle, 0, _lib.ptr(rows), _lib.ptr(out), _lib.stream_ptr()),
                    "hodg_modal_transform")
-        return out[: self.n, : N_VARS * self.nb].reshape(self.n, N_VARS, self.nb)
+        # a fresh buffer: a view of it never aliases the caller's rows
+        return out[: self.n, : N_VARS * self.nb].reshape(self.n, N_VARS, self.nb).contiguous()
 
     # -- kernels -----------------------------------------------------------
     def reset_errors(self):
@@ -295,7 +299,7 @@ def project_initial(mesh: TetMesh, geo: DeviceGeometry, field, gas: GasModel, de
     disc = _get_disc(mesh, geo, gas, BoundaryConditions(Conserved(1.0, 0.0, 0.0, 0.0, 1.0)))
     rows = disc.new_state()
     rows[: mesh.n_cells, : N_VARS * t.nb] = torch.from_numpy(ref.reshape(mesh.n_cells, -1)).to(disc.device)
-    return DofState(disc.from_reference(rows).clone())
+    return DofState(disc.from_reference(rows))
 
 
 def face_flux_pass(state: DofState, aux, mesh: TetMesh, geo: DeviceGeometry, bcs: BoundaryConditions,

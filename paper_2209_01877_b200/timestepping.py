@@ -223,7 +223,7 @@ class Stepper:
         self.init_dt()
 
     def state(self, iteration=0) -> DofState:
-        return DofState(self.disc.from_reference(self.A).clone(), iteration)
+        return DofState(self.disc.from_reference(self.A), iteration)
 
     def init_dt(self):
         """CFL dt of the loaded state into the current slot / vector."""
