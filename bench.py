@@ -117,7 +117,7 @@ def build_case(n, order, renumber, device, case="cube"):
         # freestream at Mach 0.5 and 3 degrees incidence
         mesh = P.generate_wing_box(n, device=device)
         gas = P.GasModel()
-        geo = P.compute_geometry(mesh, order)
+        geo = P.compute_geometry(mesh, order, device=device)
         bcs = P.BoundaryConditions(P.freestream_conserved(gas, 0.5, 3.0))
         state = P.project_initial(mesh, geo, lambda x, y, z: P.freestream_primitive(gas, 0.5, 3.0), gas)
         return P, mesh, gas, geo, bcs, state, None
@@ -134,7 +134,7 @@ def build_case(n, order, renumber, device, case="cube"):
         bw = (P.bandwidth(g), P.bandwidth(g, perm))
         mesh = P.apply_permutation(mesh, perm, device="cuda")  # face re-sort on the GPU
     gas = P.GasModel()
-    geo = P.compute_geometry(mesh, order)
+    geo = P.compute_geometry(mesh, order, device=device)  # element records on the GPU
     bcs = P.BoundaryConditions(P.freestream_conserved(gas, 0.5, 0.0))
     state = P.project_initial(mesh, geo, lambda x, y, z: P.vortex_primitive(gas, 0.5, 0.0, 5.0, 5.0, 5.0, 0.0, x, y),
                               gas)

@@ -189,6 +189,19 @@ int hodg_mesh_setup(int64_t n_nodes, int64_t n_elems, const double* X, const int
                     int32_t* cell_faces, int8_t* cell_fsign, int32_t* cell_neighbors, double* cell_volume,
                     double* cell_centroid, double* cell_h, int64_t* n_faces_out, void* work, void* stream);
 
+/* Element geometry records on the GPU (the device
+ * twin of paper_2209_01877_b200/geometry.py:compute_geometry, which replaces
+ * the reference's per-cell tables, hodg/geometry.py:120-220).  Inputs
+ * (device): X (n_nodes, 3), tets (n, 4) ascending rows, cell_volume, cell_h
+ * (n,), face_area (F,), cell_faces (n, 4), cell_fsign (n, 4) int8 -- the
+ * hodg_mesh_setup outputs.  Outputs: egeo tile-major (ceil(n/T), 16, T) with
+ * T = hodg_elem_tile(order) (zero padded here), econv (n, 18); flag is one
+ * device int32 of scratch.  Synchronous.  HODG_ETOPOLOGY: a degenerate
+ * element (zero Jacobian determinant). */
+int hodg_element_records(int64_t n_elems, int order, const double* X, const int32_t* tets, const double* cell_volume,
+                         const double* cell_h, const double* face_area, const int32_t* cell_faces,
+                         const int8_t* cell_fsign, double* egeo, double* econv, int32_t* flag, void* stream);
+
 /* Multi-GPU plumbing (csrc/halo.cu).
  *
  * hodg_partition_rcb: host function.  Part id per point by recursive

@@ -15,6 +15,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("HODG_B200_LIB") or os.path.join(_HERE, "_build", "libhodg_b200.so")
 
 HODG_OK, HODG_EINVAL, HODG_ECUDA, HODG_ENODEV = 0, 2, 3, 4
+HODG_ETOPOLOGY = 5
 PREC_F64, PREC_MIXED = 64, 32
 FLUX_ROE, FLUX_LLF = 0, 1
 BC_CODES = {"far_field": 1, "slip_wall": 2, "no_slip_wall": 3}
@@ -84,6 +85,7 @@ SIGNATURES = {
     "hodg_partition_rcb": (I32, [I64, P, I32, P]),
     "hodg_mesh_setup_work_bytes": (I64, [I64]),
     "hodg_mesh_setup": (I32, [I64, I64] + [P] * 16),
+    "hodg_element_records": (I32, [I64, I32] + [P] * 11),
     "hodg_halo_unique_id": (I32, [P]),
     "hodg_halo_create": (I32, [I32, I32, P, I32, P, P, P, P, P, I32, C.POINTER(C.c_void_p)]),
     "hodg_halo_exchange": (I32, [P, P, P]),

@@ -190,6 +190,62 @@ size_t carve(int64_t n, char* base, Work* w) {
     return off + 256;
 }
 
+
+// Element geometry records and modal-transform maps on the GPU: the device
+// twin of paper_2209_01877_b200/geometry.py:compute_geometry (egeo, econv),
+// which replaces the reference's per-cell tables (hodg/geometry.py:120-220).
+// J[d][k] = (V_{k+1} - V_0)[d]; J^-1 by the adjugate over the determinant
+// (the host build uses LAPACK's LU: the two agree to a few ulp).  fc, J/h and
+// J^-1 h are single roundings in numpy's order, bit-identical to the host's
+// given the same J^-1.  egeo is tile-major [tile][16][T]; the caller zeroes it.
+__global__ void elem_record_kernel(int64_t n, int T, const double* __restrict__ X, const int32_t* __restrict__ tets,
+                                   const double* __restrict__ vol, const double* __restrict__ hh,
+                                   const double* __restrict__ farea, const int32_t* __restrict__ cell_faces,
+                                   const int8_t* __restrict__ fsign, double* __restrict__ egeo,
+                                   double* __restrict__ econv, int* __restrict__ bad) {
+    const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= n) return;
+    double V[4][3];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) V[k][d] = X[int64_t(tets[e * 4 + k]) * 3 + d];
+    double J[3][3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) J[d][k] = V[k + 1][d] - V[0][d];
+    double C[3][3];  // cofactors
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            const int i1 = (i + 1) % 3, i2 = (i + 2) % 3, j1 = (j + 1) % 3, j2 = (j + 2) % 3;
+            C[i][j] = J[i1][j1] * J[i2][j2] - J[i1][j2] * J[i2][j1];
+        }
+    const double det = J[0][0] * C[0][0] + J[0][1] * C[0][1] + J[0][2] * C[0][2];
+    if (!(fabs(det) > 0.0)) {
+        atomicMax(bad, 3);
+        return;
+    }
+    const double h = hh[e], v = vol[e];
+    const int64_t base = (e / T) * 16 * T + (e % T);
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            const double ji = C[j][i] / det;
+            egeo[base + (i * 3 + j) * int64_t(T)] = ji;
+            econv[e * 18 + i * 3 + j] = J[i][j] / h;
+            econv[e * 18 + 9 + i * 3 + j] = ji * h;
+        }
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+        egeo[base + (9 + s) * int64_t(T)] = double(fsign[e * 4 + s]) * farea[cell_faces[e * 4 + s]] / v;
+    egeo[base + 13 * int64_t(T)] = h;
+    egeo[base + 14 * int64_t(T)] = v;
+}
+
 }  // namespace
 
 extern "C" {
@@ -250,6 +306,28 @@ int hodg_mesh_setup(int64_t n_nodes, int64_t n_elems, const double* X, const int
     if (cudaStreamSynchronize(st) != cudaSuccess) return HODG_ECUDA;
     hodg_count_launch(9);
     *n_faces_out = bad ? -int64_t(bad) : nf;
+    return bad ? HODG_ETOPOLOGY : HODG_OK;
+}
+
+int hodg_element_records(int64_t n_elems, int order, const double* X, const int32_t* tets, const double* cell_volume,
+                         const double* cell_h, const double* face_area, const int32_t* cell_faces,
+                         const int8_t* cell_fsign, double* egeo, double* econv, int32_t* flag, void* stream) {
+    if (n_elems <= 0 || !X || !tets || !cell_volume || !cell_h || !face_area || !cell_faces || !cell_fsign || !egeo ||
+        !econv || !flag)
+        return HODG_EINVAL;
+    const int T = hodg_elem_tile(order);
+    if (T <= 0) return HODG_EINVAL;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t nt = (n_elems + T - 1) / T;
+    if (cudaMemsetAsync(egeo, 0, size_t(nt) * 16 * T * sizeof(double), st) != cudaSuccess ||
+        cudaMemsetAsync(flag, 0, sizeof(int32_t), st) != cudaSuccess)
+        return HODG_ECUDA;
+    elem_record_kernel<<<nb(n_elems), TPB, 0, st>>>(n_elems, T, X, tets, cell_volume, cell_h, face_area, cell_faces,
+                                                    cell_fsign, egeo, econv, reinterpret_cast<int*>(flag));
+    hodg_count_launch(1);
+    int bad = 0;
+    cudaMemcpyAsync(&bad, flag, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return HODG_ECUDA;
     return bad ? HODG_ETOPOLOGY : HODG_OK;
 }
 

@@ -66,6 +66,15 @@ def tile_major(a: np.ndarray, tile: int) -> np.ndarray:
     return np.ascontiguousarray(pad.reshape(nt, tile, nf).transpose(0, 2, 1)).ravel()
 
 
+def _devkey(device) -> str:
+    import torch
+
+    d = torch.device(device)
+    if d.type == "cuda" and d.index is None:
+        d = torch.device("cuda", torch.cuda.current_device())
+    return str(d)
+
+
 class GeometryError(Exception):
     pass
 
@@ -99,15 +108,18 @@ class DeviceGeometry:
         """Device copies (torch tensors), uploaded once per device."""
         import torch
 
-        d = self._dev.get(str(device))
-        if d is None:
-            d = {k: torch.from_numpy(np.ascontiguousarray(getattr(self, k))).to(device)
-                 for k in ("egeo", "econv", "efaces", "fcells", "finfo", "fnrm")}
-            self._dev[str(device)] = d
+        d = self._dev.setdefault(_devkey(device), {})
+        for k in ("egeo", "econv", "efaces", "fcells", "finfo", "fnrm"):
+            if k not in d:
+                d[k] = torch.from_numpy(np.ascontiguousarray(getattr(self, k))).to(device)
         return d
 
     def constant_count(self) -> int:
-        return sum(getattr(self, k).size for k in ("egeo", "econv", "fnrm"))
+        n = 0
+        for k in ("egeo", "econv", "fnrm"):
+            a = getattr(self, k)
+            n += a.size if a is not None else next(d[k].numel() for d in self._dev.values() if k in d)
+        return n
 
 
 def element_jacobians(mesh: TetMesh):
@@ -116,18 +128,24 @@ def element_jacobians(mesh: TetMesh):
     return V, J
 
 
-def compute_geometry(mesh: TetMesh, order: int, split: int | None = None) -> DeviceGeometry:
+def compute_geometry(mesh: TetMesh, order: int, split: int | None = None, device=None) -> DeviceGeometry:
     """Device geometry.  Faces are laid out [interior | boundary | interior
     tail]: mesh faces [0, split) split into interior then boundary faces
     (order kept within each class), mesh faces [split, F) -- a partition's
     ghost faces, all interior -- after them; the interior ranges run the
-    face-kernel variant without boundary-state code."""
+    face-kernel variant without boundary-state code.
+
+    device="cuda": the element records (egeo, econv) are built on the GPU by
+    hodg_element_records and kept there only (geo.egeo / geo.econv are None);
+    J^-1 agrees with the host's LAPACK inverse to a few ulp."""
     if order not in (0, 1, 2, 3):
         raise GeometryError(f"unsupported order {order}; expected 0..3")
     codes = mesh.boundary_kind_codes()
     if np.any(codes < 0):
         raise GeometryError(f"boundary face {int(np.flatnonzero(codes < 0)[0])} has no boundary patch")
     n = mesh.n_cells
+    if device is not None:
+        return _with_face_layout(mesh, order, split, codes, None, None, _device_records(mesh, order, device))
     V, J = element_jacobians(mesh)
     det = np.linalg.det(J)
     if np.any(np.abs(det) <= 0.0):
@@ -144,6 +162,36 @@ def compute_geometry(mesh: TetMesh, order: int, split: int | None = None) -> Dev
     econv = np.empty((n, 18))
     econv[:, 0:9] = (J / h[:, None, None]).reshape(n, 9)
     econv[:, 9:18] = (Jinv * h[:, None, None]).reshape(n, 9)
+    return _with_face_layout(mesh, order, split, codes, egeo, econv, None)
+
+
+def _device_records(mesh: TetMesh, order: int, device):
+    """(egeo, econv) device tensors from hodg_element_records."""
+    import torch
+
+    from . import _lib
+
+    L = _lib.lib()
+    dev = torch.device(device)
+    n, T = mesh.n_cells, TILE[order]
+    up = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev)  # noqa: E731
+    X = up(mesh.node_xy, np.float64)
+    tets = up(mesh.cell_nodes, np.int32)
+    vol, h = up(mesh.cell_area, np.float64), up(mesh.cell_h, np.float64)
+    area = up(mesh.face_length, np.float64)
+    cf, fs = up(mesh.cell_faces, np.int32), up(mesh.cell_fsign, np.int8)
+    egeo = torch.empty(((n + T - 1) // T) * 16 * T, dtype=torch.float64, device=dev)
+    econv = torch.empty((n, 18), dtype=torch.float64, device=dev)
+    flag = torch.empty(1, dtype=torch.int32, device=dev)
+    rc = L.hodg_element_records(n, order, *[_lib.ptr(t) for t in (X, tets, vol, h, area, cf, fs, egeo, econv, flag)],
+                                _lib.stream_ptr())
+    if rc == _lib.HODG_ETOPOLOGY:
+        raise GeometryError("degenerate element")
+    _lib.check(rc, "hodg_element_records")
+    return {"egeo": egeo, "econv": econv}
+
+
+def _with_face_layout(mesh, order, split, codes, egeo, econv, dev_records):
     F = mesh.n_faces
     split = F if split is None else int(split)
     ids = np.arange(F)
@@ -161,9 +209,12 @@ def compute_geometry(mesh: TetMesh, order: int, split: int | None = None) -> Dev
     T = TILE[order]
     efaces = inv[mesh.cell_faces.astype(np.int64)].astype(np.int32)
     efaces[mesh.cell_faces < 0] = 0
-    return DeviceGeometry(order, ref_tables(order).nb, tile_major(egeo, T), econv, tile_major(efaces, T),
-                          mesh.face_cells.astype(np.int32)[perm], finfo, fnrm, perm, inv,
-                          int(np.count_nonzero(~bnd[:split])), int(np.count_nonzero(bnd[:split])))
+    geo = DeviceGeometry(order, ref_tables(order).nb, None if egeo is None else tile_major(egeo, T), econv,
+                         tile_major(efaces, T), mesh.face_cells.astype(np.int32)[perm], finfo, fnrm, perm, inv,
+                         int(np.count_nonzero(~bnd[:split])), int(np.count_nonzero(bnd[:split])))
+    if dev_records is not None:
+        geo._dev[_devkey(dev_records["egeo"].device)] = dict(dev_records)
+    return geo
 
 
 def volume_points(mesh: TetMesh, order: int) -> np.ndarray:

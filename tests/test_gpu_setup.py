@@ -68,3 +68,55 @@ def test_device_setup_c1m_time():
     print(f"C1M build: host {t1 - t0:.2f} s, device {t2 - t1:.2f} s ({host.n_cells} tets, {host.n_faces} faces)")
     assert dev.n_faces == host.n_faces == 2014650
     assert np.array_equal(dev.cell_faces, host.cell_faces)
+
+
+@pytest.mark.parametrize("order", [1, 2, 3])
+def test_device_element_records_equal_host(order):
+    """hodg_element_records vs compute_geometry's numpy/LAPACK build: fc, h,
+    vol and J/h bit-identical, J^-1 (adjugate vs LU) to a few ulp; face
+    layout identical; an FP64 residual through either geometry agrees."""
+    import torch
+
+    import paper_2209_01877_b200 as P
+
+    m = M.perturb_interior_nodes(M.generate_tet_box(5, 4, 3, bc={"xmin": "far_field", "xmax": "far_field",
+                                                                 "ymin": "slip_wall", "ymax": "slip_wall",
+                                                                 "zmin": "no_slip_wall", "zmax": "far_field"}),
+                                 0.15, seed=3)
+    host = P.compute_geometry(m, order)
+    dev = P.compute_geometry(m, order, device="cuda")
+    assert dev.egeo is None and dev.econv is None
+    for k in ("efaces", "fcells", "finfo", "fnrm", "face_perm", "face_inv"):
+        assert np.array_equal(getattr(host, k), getattr(dev, k)), k
+    assert (host.n_int0, host.n_bnd) == (dev.n_int0, dev.n_bnd)
+    d = dev.device("cuda")
+    from paper_2209_01877_b200.geometry import TILE
+
+    T = TILE[order]
+    eg = d["egeo"].cpu().numpy().reshape(-1, 16, T)
+    hg = host.egeo.reshape(-1, 16, T)
+    assert np.array_equal(eg[:, 9:, :], hg[:, 9:, :])
+    scale = np.abs(hg[:, :9, :]).max(axis=1, keepdims=True)  # per element (0 on padding lanes)
+    assert np.all(np.abs(eg[:, :9, :] - hg[:, :9, :]) <= 1e-14 * scale)
+    ec = d["econv"].cpu().numpy()
+    assert np.array_equal(ec[:, :9], host.econv[:, :9])
+    assert np.allclose(ec[:, 9:], host.econv[:, 9:], rtol=0, atol=1e-14 * np.abs(host.econv[:, 9:]).max())
+    assert dev.constant_count() == host.constant_count()
+    gas = P.GasModel()
+    bcs = P.BoundaryConditions(P.freestream_conserved(gas, 0.4, 10.0))
+    rng = np.random.default_rng(order)
+    st = P.project_initial(m, host, lambda x, y, z: P.vortex_primitive(gas, 0.4, 10.0, 0.5, 0.5, 0.5, 0.0, x, y), gas)
+    c = st.coeffs.cpu().numpy() * (1.0 + 0.01 * rng.standard_normal(st.coeffs.shape))
+    r_h = P.rhs(P.DofState(torch.from_numpy(c).cuda()), m, host, bcs, gas).res.cpu().numpy()
+    r_d = P.rhs(P.DofState(torch.from_numpy(c).cuda()), m, dev, bcs, gas).res.cpu().numpy()
+    assert np.linalg.norm(r_d - r_h) <= 1e-13 * np.linalg.norm(r_h)
+
+
+def test_device_element_records_reject_degenerate():
+    import paper_2209_01877_b200 as P
+    from paper_2209_01877_b200.geometry import GeometryError
+
+    m = M.generate_tet_box(2, 2, 2)
+    m.node_xy[:, 2] = 0.0  # flatten every element
+    with pytest.raises(GeometryError):
+        P.compute_geometry(m, 1, device="cuda")
