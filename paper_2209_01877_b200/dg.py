@@ -229,21 +229,30 @@ class Discretization:
         if kind == 3:
             raise AdmissibilityError("inadmissible cell mean", cell=int(idv.value), iteration=iteration)
 
-    def face_flux(self, rows, prec, hbuf=None, stream=None, f_begin=0, f_end=None):
-        """Face kernel over device faces [f_begin, f_end): interior ranges use
-        the kernel variant without boundary states, the boundary range the
-        general one."""
-        hbuf = self.face_buffer(prec) if hbuf is None else hbuf
+    def face_segments(self, f_begin=0, f_end=None):
+        """The face-kernel launches over [f_begin, f_end): (lo, hi, interior_only)."""
         f_end = self.nf if f_end is None else f_end
         g = self.geo
         b0, b1 = g.n_int0, g.n_int0 + g.n_bnd
-        for lo, hi, interior in ((0, b0, 1), (b0, b1, 0), (b1, self.nf, 1)):
-            lo, hi = max(lo, f_begin), min(hi, f_end)
-            if hi > lo:
-                fn = self.L.hodg_face_flux_range_es if hbuf.dim() == 1 else self.L.hodg_face_flux_range
-                _lib.check(fn(self.handle, prec, _lib.ptr(rows), _lib.ptr(hbuf), int(lo),
-                                                       int(hi), interior, _lib.ptr(self.err),
-                                                       _lib.stream_ptr(stream)), "hodg_face_flux_range")
+        segs = [(max(lo, f_begin), min(hi, f_end), interior)
+                for lo, hi, interior in ((0, b0, 1), (b0, b1, 0), (b1, self.nf, 1))]
+        segs = [sg for sg in segs if sg[1] > sg[0]]
+        if len(segs) >= 2 and segs[-2][2] == 0:
+            # boundary range + partition tail: one launch of the general
+            # variant (it treats interior faces exactly as the interior one)
+            segs[-2:] = [(segs[-2][0], segs[-1][1], 0)]
+        return segs
+
+    def face_flux(self, rows, prec, hbuf=None, stream=None, f_begin=0, f_end=None):
+        """Face kernel over device faces [f_begin, f_end): interior ranges use
+        the kernel variant without boundary states, the boundary range the
+        general one (extended over a partition tail that follows it: one
+        launch fewer)."""
+        hbuf = self.face_buffer(prec) if hbuf is None else hbuf
+        for lo, hi, interior in self.face_segments(f_begin, f_end):
+            fn = self.L.hodg_face_flux_range_es if hbuf.dim() == 1 else self.L.hodg_face_flux_range
+            _lib.check(fn(self.handle, prec, _lib.ptr(rows), _lib.ptr(hbuf), int(lo), int(hi), interior,
+                          _lib.ptr(self.err), _lib.stream_ptr(stream)), "hodg_face_flux_range")
         return hbuf
 
     def stage(self, prec, hbuf, args: _lib.StageArgs, stream=None):

@@ -88,7 +88,9 @@ class DistributedStepper(Stepper):
 
         d = self.disc
         n_st = len(SCHEMES[self.scheme])
-        ni = self.part.n_inner_faces
+        # faces are [interior | boundary | partition]: the interior ones
+        # overlap the exchange; boundary + partition faces are one launch
+        ni = d.geo.n_int0
         for k in range(n_st):
             us = self.A if k == 0 else self.B
             self.halo.start(us)
@@ -111,7 +113,10 @@ class DistributedStepper(Stepper):
             self.norms.copy_(torch.sqrt(self.norm_sums))
 
     def launches_per_step(self) -> int:
-        return 3 * len(SCHEMES[self.scheme])
+        d = self.disc
+        ni = d.geo.n_int0
+        per_stage = len(d.face_segments(0, ni)) + len(d.face_segments(ni, d.nf)) + 1
+        return per_stage * len(SCHEMES[self.scheme])  # (the norm sums are torch reductions here)
 
     def close(self):
         """Release the exchange (the native one owns an NCCL communicator);

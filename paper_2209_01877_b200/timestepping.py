@@ -300,7 +300,10 @@ class Stepper:
         d.residual_rows(self.A, self.hbuf, self.prec, res=self.B)
 
     def launches_per_step(self) -> int:
-        return 2 * len(SCHEMES[self.scheme]) + (1 if self.log_norms else 0)
+        """Kernels one step launches: per stage the face-kernel ranges and the
+        element kernel, plus the norm finalize."""
+        per_stage = len(self.disc.face_segments()) + 1
+        return per_stage * len(SCHEMES[self.scheme]) + (1 if self.log_norms else 0)
 
     def step(self):
         """Advance one step (asynchronous; no host sync)."""
