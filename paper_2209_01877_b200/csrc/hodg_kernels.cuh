@@ -7,6 +7,7 @@
 // tables (hodg/geometry.py:33-51) collapse into compile-time constants and
 // the per-element data is 16 doubles (J^-1, sgn*area/vol per face, h, vol).
 
+#include <cstdlib>
 #include <utility>
 
 #include "hodg_common.cuh"
@@ -71,6 +72,14 @@ constexpr int ETHREADS = 5 * E * H;
 #ifndef HODG_PDL_MAX_ELEMS
 #define HODG_PDL_MAX_ELEMS 200000
 #endif
+// the element bound, overridable at run time (env HODG_PDL_MAX_ELEMS; 0 = never)
+inline int64_t hodg_pdl_max_elems() {
+    static const int64_t v = [] {
+        const char* s = getenv("HODG_PDL_MAX_ELEMS");
+        return s ? int64_t(strtoll(s, nullptr, 10)) : int64_t(HODG_PDL_MAX_ELEMS);
+    }();
+    return v;
+}
 #ifndef HODG_EMINB
 #define HODG_EMINB 0
 #endif
@@ -955,7 +964,7 @@ static int launch_face_k(const hodg_mesh_desc& m, const double* state, void* hbu
     const int64_t ntiles = (fe - fb + FT - 1) / FT;
     const int64_t nblk = ntiles < grid_cap ? ntiles : grid_cap;  // persistent CTAs loop over tiles
     if (nblk > 0) {
-        if (HODG_PDL && m.n_elems <= HODG_PDL_MAX_ELEMS) {
+        if (HODG_PDL && m.n_elems <= hodg_pdl_max_elems()) {
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3(unsigned(nblk));
             cfg.blockDim = dim3(FACE_THREADS);
@@ -1002,7 +1011,7 @@ static int launch_elem_k(const hodg_mesh_desc& m, const void* hbuf, const hodg_s
     }
     const int64_t nblk = (m.n_elems + E - 1) / E;
     if (nblk > 0) {
-        if (HODG_PDL && m.n_elems <= HODG_PDL_MAX_ELEMS) {
+        if (HODG_PDL && m.n_elems <= hodg_pdl_max_elems()) {
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3(unsigned(nblk));
             cfg.blockDim = dim3(ETHREADS);
