@@ -255,6 +255,23 @@ class Discretization:
                           _lib.ptr(self.err), _lib.stream_ptr(stream)), "hodg_face_flux_range")
         return hbuf
 
+    def face_flux_split(self, rows, prec, hbuf, side):
+        """face_flux over all faces with the boundary (+ partition) range on
+        the `side` stream, issued after the interior range: its CTAs take the
+        SM slots the persistent interior kernel frees in its tail instead of
+        running as a separate, mostly-ramp launch afterwards.  Joined back
+        into the current stream."""
+        torch = _torch()
+        segs = self.face_segments()
+        if side is None or len(segs) < 2:
+            return self.face_flux(rows, prec, hbuf)
+        cur = torch.cuda.current_stream()
+        side.wait_stream(cur)
+        self.face_flux(rows, prec, hbuf, f_begin=segs[0][0], f_end=segs[0][1])
+        self.face_flux(rows, prec, hbuf, stream=side, f_begin=segs[1][0], f_end=self.nf)
+        cur.wait_stream(side)
+        return hbuf
+
     def stage(self, prec, hbuf, args: _lib.StageArgs, stream=None):
         fn = self.L.hodg_elem_stage_es if hbuf.dim() == 1 else self.L.hodg_elem_stage
         _lib.check(fn(self.handle, prec, _lib.ptr(hbuf), C.byref(args), _lib.ptr(self.err),

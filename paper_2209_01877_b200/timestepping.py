@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -213,6 +214,8 @@ class Stepper:
         self.steps = 0
         self._graphs = {}
         self._args = []
+        # boundary faces concurrent with the interior tail (HODG_OVERLAP_BND=0: serial)
+        self._side = torch.cuda.Stream(device=dev) if os.environ.get("HODG_OVERLAP_BND", "1") != "0" else None
         self.capture_mode = "global"
 
     # -- state in / out ----------------------------------------------------
@@ -284,7 +287,7 @@ class Stepper:
         n_st = len(SCHEMES[self.scheme])
         for k in range(n_st):
             us = self.A if k == 0 else self.B
-            d.face_flux(us, self.prec, self.hbuf)
+            d.face_flux_split(us, self.prec, self.hbuf, self._side)
             args = self._stage_args(k, parity)
             self._args.append(args)
             d.stage(self.prec, self.hbuf, args)

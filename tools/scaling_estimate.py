@@ -70,6 +70,9 @@ def main():
         lgeo = compute_geometry(part.mesh, args.order, split=part.n_inner_faces)
         d = Discretization(part.mesh, lgeo, gas, bcs, n_elems=part.n_owned)
         st = Stepper(d, "rk3", 64, "global", 0.3, use_graph=True)
+        # the DistributedStepper's schedule: boundary + partition faces after
+        # the interior ones (they wait for the halo), not on a side stream
+        st._side = None
         gl = torch.as_tensor(np.concatenate([part.owned, part.ghosts]), device="cuda")
         st.A.copy_(rows_g.index_select(0, gl))
         st.init_dt()
