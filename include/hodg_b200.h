@@ -138,9 +138,11 @@ int hodg_elem_stage(const hodg_mesh* mesh, int prec, const void* face_buf, const
 /* Element-slot record layout (the stepper's fused path; same values as
  * face_buf, different placement): block e holds the records of element e's
  * four faces, slot-major, 5 x NQF values each ([slot][var][qp]), at stride
- * hodg_elem_record_stride(order) = 20 NQF + 1 values (odd: conflict-free
- * per-element smem reads; a tile of hodg_elem_tile(order) blocks is one 16-byte
- * multiple, fetched with one TMA bulk copy).  The face kernel stores each
+ * hodg_elem_record_stride(order) = 20 NQF + 1 values for the CTA element
+ * kernel (odd: conflict-free per-element smem reads) or 20 NQF + 2 for the
+ * warp-group kernel (P1, and P2 when built with it); a tile of
+ * hodg_elem_tile(order) blocks is a 16-byte multiple at either precision,
+ * fetched with one TMA bulk copy.  The face kernel stores each
  * face's record into the blocks of both neighbours (owned elements only:
  * id < n_elems), so the element kernel needs no per-face gather.  Buffer:
  * hodg_elem_record_len(mesh, prec) values at the kernel precision. */

@@ -411,6 +411,11 @@ class RunSpec:
     log_every: int = 1
     precision_mode: str = "dp"
     switch_iter: int = 0
+    window: int = 200
+    factor: float = 2.0
+    dt_floor: float = 0.0
+    dt_fixed: float | None = None
+    t_final: float | None = None
     scheme: str = "rk2"  # rk2 | rk3
     flux_kind: int = 0  # 0 Roe (Harten-Hyman), 1 LLF
     state_bits_mp: int = 32  # storage width during reduced-precision steps
@@ -422,6 +427,9 @@ class History:
     res: list = field(default_factory=list)
     dts: list = field(default_factory=list)
     precision: list = field(default_factory=list)
+    t_sim: float = 0.0  # simulated time (global dt mode)
+    switch: int | None = None  # iteration of the promotion to 64-bit
+
 
 
 def initial_state(spec, disc):
@@ -447,7 +455,7 @@ def run(spec: RunSpec):
     disc = Disc(m, compute_tables(m, spec.order), spec.gas,
                 freestream_conserved(spec.gas, spec.mach, spec.angle_deg, m.dim), spec.flux_kind)
     u = initial_state(spec, disc)
-    ctrl = PrecisionController(spec.precision_mode, spec.switch_iter)
+    ctrl = PrecisionController(spec.precision_mode, spec.switch_iter, spec.window, spec.factor)
     hist = History()
     if ctrl.starts_reduced():
         u32 = u.astype(np.float32)
@@ -457,11 +465,20 @@ def run(spec: RunSpec):
     step = rk3_step if spec.scheme == "rk3" else rk2_step
     for it in range(spec.max_iterations):
         bits = ctrl.decide(it, [r[0] for r in hist.res])
+        if bits == 64 and hist.switch is None and ctrl._switched:
+            hist.switch = it
         if bits == 64 and u.dtype == np.float32:
             u = u.astype(np.float64)
         dts = local_dt_field(disc, u, spec.cfl, spec.order, it)
+        # hodg/timestepping.py:328-341: dt floor, fixed dt, t_final clip
+        if spec.dt_floor > 0.0:
+            np.maximum(dts, spec.dt_floor, out=dts)
         if spec.dt_mode == "global":
-            dt = min_reduce(dts)
+            dt = spec.dt_fixed if spec.dt_fixed is not None else min_reduce(dts)
+            if spec.t_final is not None:
+                if hist.t_sim >= spec.t_final - 1e-14:
+                    break
+                dt = min(dt, spec.t_final - hist.t_sim)
             dtv = np.full(m.n_cells, dt)
             dt_log = dt
         else:
@@ -476,6 +493,8 @@ def run(spec: RunSpec):
             return r
 
         u = step(u, dtv, rfn)
+        if spec.dt_mode == "global":
+            hist.t_sim += dt_log
         if spec.log_every and (it % spec.log_every == 0 or it == spec.max_iterations - 1):
             res4 = residual_l2(first[0], m.cell_area)
             if not np.all(np.isfinite(res4)):

@@ -78,6 +78,15 @@ __device__ __forceinline__ void bulk_wait_read() {
 }
 
 
+// 16-byte global -> shared copy by the calling thread (cp.async, L2 only);
+// completion per thread with cp_async_wait_all(), then a barrier among the
+// threads that read the destination
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 // make generic-proxy smem writes visible to the async (TMA) proxy
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

@@ -58,7 +58,25 @@ constexpr int H = (ORDER == 3) ? HODG_H3 : (ORDER == 2 ? HODG_H2 : 1);
 #ifndef HODG_E1
 #define HODG_E1 32
 #endif
-constexpr int E = (ORDER >= 3) ? (H > 1 ? 32 : 16) : (ORDER == 2 ? HODG_E2 : (ORDER == 1 ? HODG_E1 : 64));
+// P1 and P2 run the warp-group element kernel (hodg_elem_warp.cuh): G = 6
+// elements per warp, lane (e, v); its element tile is the warp's group
+#ifndef HODG_WARP_ELEM_P1
+#define HODG_WARP_ELEM_P1 1
+#endif
+#ifndef HODG_WARP_ELEM_P2
+#define HODG_WARP_ELEM_P2 0
+#endif
+constexpr bool WARP_ELEM = (ORDER == 1 && HODG_WARP_ELEM_P1) || (ORDER == 2 && HODG_WARP_ELEM_P2);
+// volume integral of the CTA element kernel through the moments of the
+// physical flux (hodg_elem_warp.cuh explains the identity); H == 1 only
+#ifndef HODG_MOMENTS
+#define HODG_MOMENTS 1
+#endif
+constexpr int NBL = ORDER * (ORDER + 1) * (ORDER + 2) / 6;  // monomials of degree < ORDER
+constexpr bool MOMENTS = HODG_MOMENTS && H == 1 && ORDER >= 1;
+constexpr int G = 6;
+constexpr int E = WARP_ELEM ? G
+                            : ((ORDER >= 3) ? (H > 1 ? 32 : 16) : (ORDER == 2 ? HODG_E2 : (ORDER == 1 ? HODG_E1 : 64)));
 constexpr int NH = NB / H;
 static_assert(NB % H == 0 && (H == 1 || E >= 32) && 5 * H <= 15, "basis split layout");
 constexpr int ETHREADS = 5 * E * H;
@@ -116,8 +134,10 @@ __host__ __device__ constexpr int hsmem() {
 // values each, slot-major, unpadded) plus one pad value, so the stride is
 // odd (conflict-free per-element smem access) and an E-element tile is a
 // 16-byte multiple (one TMA bulk copy per tile)
+// (warp-group kernel: even, so a 6-element group of FP32 blocks is a 16-byte
+// multiple)
 constexpr int HSE = 5 * NQF;
-constexpr int EREC = 4 * HSE + 1;
+constexpr int EREC = WARP_ELEM ? 4 * HSE + 2 : 4 * HSE + 1;
 
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 __host__ __device__ constexpr size_t cmax(size_t a, size_t b) { return a > b ? a : b; }
@@ -217,6 +237,50 @@ __device__ __forceinline__ void hsel(int h, F&& f) {
 }
 
 // ---------------------------------------------------------------------------
+// Face gather of one local face s: fa[i] = sum_q FG[s][q][i0 + i] h[q] for
+// this thread's basis functions [i0, i0 + N).  On faces s = 1, 2, 3 the
+// coordinate eta_{s-1} is -1/4 at every point (the face opposite vertex s of
+// the reference tetrahedron has xi_{s-1} = 0), so the weighted trace of a
+// monomial with exponent c > 0 in that coordinate is (-1/4)^c times the
+// trace of the monomial without it: exactly, since the factor is a power of
+// two (refelem.py builds the tables as products).  Only the c = 0 monomials
+// are contracted (P2: 6 of 10, P3: 10 of 20); the rest are one scaling each
+// and equal the direct contraction bit for bit.
+template <typename T, int S, int I0, int N, int NQ>
+__device__ __forceinline__ void face_moments(const T (&hq)[NQ], T (&fa)[N]) {
+    constexpr int d = S - 1;
+    sfor<N>([&](auto i) {
+        constexpr int ig = I0 + i;
+        constexpr bool direct = S == 0 || expt(ig, d < 0 ? 0 : d) == 0;
+        if constexpr (direct) {
+            T x = T(0);
+            sfor<NQ>([&](auto q) { x += TAB(FG, T, (S * NQ + q) * NB + ig) * hq[q]; });
+            fa[i] = x;
+        }
+    });
+    if constexpr (S > 0) {
+        sfor<N>([&](auto i) {
+            constexpr int ig = I0 + i;
+            constexpr int c = expt(ig, d);
+            if constexpr (c > 0) {
+                constexpr int base = mono_index(expt(ig, 0) - (d == 0 ? c : 0), expt(ig, 1) - (d == 1 ? c : 0),
+                                                expt(ig, 2) - (d == 2 ? c : 0));
+                static_assert(base >= I0 && base < I0 + N || N != NB, "full basis per thread holds the base");
+                if constexpr (base >= I0 && base < I0 + N) {
+                    constexpr double sc = c == 1 ? -0.25 : (c == 2 ? 0.0625 : -0.015625);
+                    fa[i] = T(sc) * fa[base - I0];
+                } else {
+                    // basis split: the base function lives in the other part
+                    T x = T(0);
+                    sfor<NQ>([&](auto q) { x += TAB(FG, T, (S * NQ + q) * NB + ig) * hq[q]; });
+                    fa[i] = x;
+                }
+            }
+        });
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Face kernel: hodg/dg.py:240-351.  One CTA = FT faces.
 //  phase 0: each (face, side) thread bulk-copies its element's state row
 //           (TMA, cp.async.bulk) into shared memory;
@@ -244,7 +308,7 @@ __global__ void __launch_bounds__(FACE_THREADS, HODG_FACE_MINB) face_flux_kernel
                            sizeof(double);
     __shared__ double fn[2][FT][3];
     __shared__ int finf[2][FT];
-    __shared__ int fdst[2][FT][2];  // ES: record offsets of the left / right blocks (-1: none)
+    __shared__ int64_t fdst[2][FT][2];  // ES: record offsets of the left / right blocks (-1: none)
 
     const int t = threadIdx.x;
     const int side = t / (FT * NG);
@@ -295,9 +359,10 @@ __global__ void __launch_bounds__(FACE_THREADS, HODG_FACE_MINB) face_flux_kernel
         if (side == 0 && g == 0) {
             finf[buf][lf] = ((mt.info >> 4) & 15) | (mt.right >= 0 ? 0x100 : 0);
             if constexpr (ES) {
-                fdst[buf][lf][0] = mt.elem < m.n_elems ? mt.elem * EREC + (mt.info & 3) * HSE : -1;
-                fdst[buf][lf][1] =
-                    (mt.right >= 0 && mt.right < m.n_elems) ? mt.right * EREC + ((mt.info >> 2) & 3) * HSE : -1;
+                fdst[buf][lf][0] = mt.elem < m.n_elems ? int64_t(mt.elem) * EREC + (mt.info & 3) * HSE : -1;
+                fdst[buf][lf][1] = (mt.right >= 0 && mt.right < m.n_elems)
+                                       ? int64_t(mt.right) * EREC + ((mt.info >> 2) & 3) * HSE
+                                       : -1;
             }
             fn[buf][lf][0] = mt.nrm.x;
             fn[buf][lf][1] = mt.nrm.y;
@@ -429,14 +494,14 @@ __global__ void __launch_bounds__(FACE_THREADS, HODG_FACE_MINB) face_flux_kernel
                     for (int v = 0; v < 5; ++v) h[k][v] = T(0);
                 }
                 if constexpr (ES) {
-                    const int dl = fdst[buf][lfv[k]][0], dr = fdst[buf][lfv[k]][1];
+                    const int64_t dl = fdst[buf][lfv[k]][0], dr = fdst[buf][lfv[k]][1];
                     if (dl >= 0) {
 #pragma unroll
-                        for (int v = 0; v < 5; ++v) hbuf[int64_t(dl) + v * NQF + qv[k]] = h[k][v];
+                        for (int v = 0; v < 5; ++v) hbuf[dl + v * NQF + qv[k]] = h[k][v];
                     }
                     if (dr >= 0) {
 #pragma unroll
-                        for (int v = 0; v < 5; ++v) hbuf[int64_t(dr) + v * NQF + qv[k]] = h[k][v];
+                        for (int v = 0; v < 5; ++v) hbuf[dr + v * NQF + qv[k]] = h[k][v];
                     }
                 } else {
 #pragma unroll
@@ -560,6 +625,9 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : 4) : E
     T acc[NH];
 #pragma unroll
     for (int i = 0; i < NH; ++i) acc[i] = T(0);
+    T mom[MOMENTS ? NBL : 1][3];
+#pragma unroll
+    for (int j = 0; j < (MOMENTS ? NBL : 1); ++j) mom[j][0] = mom[j][1] = mom[j][2] = T(0);
     T ji[H == 1 ? 9 : 1];
     if constexpr (H == 1) {
 #pragma unroll
@@ -628,8 +696,23 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : 4) : E
         }
         __syncthreads();
         // phase C (volume): contravariant flux of variable v against the
-        // weighted derivative table, this part's basis functions
-        if (live) {
+        // weighted derivative table, this part's basis functions (MOMENTS:
+        // the physical flux of variable v against the weighted lower
+        // monomials; J^-1 and the derivative identity after the last chunk)
+        if constexpr (MOMENTS) {
+            if (live) {
+                sfor<nq>([&](auto qq) {
+                    const T* sl = X + (qq * E + e) * XS;
+                    const T fx = sl[v], fy = sl[5 + v], fz = sl[10 + v];
+                    sfor<NBL>([&](auto j) {
+                        const T wm = TAB(WV, T, (q0 + qq) * NB + j);
+                        mom[j][0] += wm * fx;
+                        mom[j][1] += wm * fy;
+                        mom[j][2] += wm * fz;
+                    });
+                });
+            }
+        } else if (live) {
             hsel(h, [&](auto hc) {
                 sfor<nq>([&](auto qq) {
                     const T* sl = X + (qq * E + e) * XS;
@@ -656,6 +739,26 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : 4) : E
         }
         __syncthreads();
     });
+    if constexpr (MOMENTS) {
+        // sum_q VD[q][i][d] (J^-1 F)_d = sum_d alpha_{i,d} sum_k Jinv[d][k] MOM[i - e_d][k]
+        T mj[NBL][3];
+#pragma unroll
+        for (int j = 0; j < NBL; ++j)
+#pragma unroll
+            for (int d = 0; d < 3; ++d)
+                mj[j][d] = ji[3 * d] * mom[j][0] + ji[3 * d + 1] * mom[j][1] + ji[3 * d + 2] * mom[j][2];
+        sfor<NB>([&](auto i) {
+            T sum = T(0);
+            sfor<3>([&](auto d) {
+                constexpr int al = expt(i, d);
+                if constexpr (al > 0) {
+                    constexpr int lo = mono_index(expt(i, 0) - (d == 0), expt(i, 1) - (d == 1), expt(i, 2) - (d == 2));
+                    sum += T(al) * mj[lo][d];
+                }
+            });
+            acc[i] = sum;
+        });
+    }
 
     // P3: the u0 tile is not held in registers through the volume phases;
     // one TMA copy into the freed state / X region, in flight during the
@@ -692,11 +795,7 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : 4) : E
                     for (int q = 0; q < NQF; ++q) hq[q] = hrec[q];
                 }
                 T fa[NH];
-#pragma unroll
-                for (int i = 0; i < NH; ++i) fa[i] = T(0);
-                sfor<NQF>([&](auto q) {
-                    sfor<NH>([&](auto i) { fa[i] += TAB(FG, T, (s * NQF + q) * NB + hc * NH + i) * hq[q]; });
-                });
+                face_moments<T, s, hc * NH, NH>(hq, fa);
                 const double fc = G[(9 + s) * E + e];
 #pragma unroll
                 for (int i = 0; i < NH; ++i) accd[i] -= fc * double(fa[i]);
@@ -933,6 +1032,8 @@ __global__ void modal_transform_kernel(const hodg_mesh_desc m, int to_reference,
         for (int i = 0; i < NB; ++i) out[c * RS + v * NB + i] = o[v][i];
 }
 
+#include "hodg_elem_warp.cuh"
+
 }  // namespace HODG_CAT(ord, ORDER)
 }  // namespace hodg
 
@@ -942,48 +1043,63 @@ __global__ void modal_transform_kernel(const hodg_mesh_desc m, int to_reference,
 namespace hodg {
 namespace HODG_CAT(ord, ORDER) {
 
+// per-device launch setup of one kernel: the dynamic shared memory attribute
+// and the persistent grid cap (CTAs per SM x SMs) -- a process may drive
+// several devices, so both are cached per device
+struct LaunchCache {
+    int cap[64] = {0};
+};
+template <typename K>
+static int launch_setup(LaunchCache& lc, K kernel, int threads, size_t smem, int* cap) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return HODG_ECUDA;
+    if (lc.cap[dev] == 0) {
+        if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
+            return HODG_ECUDA;
+        int sms = 0, per_sm = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+        lc.cap[dev] = sms * (per_sm > 0 ? per_sm : 1);
+    }
+    *cap = lc.cap[dev];
+    return HODG_OK;
+}
+
+// ordinary launch, or a programmatic dependent launch (griddepcontrol) on
+// meshes of at most HODG_PDL_MAX_ELEMS elements
+template <typename K, typename... Args>
+static int launch_maybe_pdl(const hodg_mesh_desc& m, K kernel, int64_t nblk, int threads, size_t smem,
+                            cudaStream_t st, Args... args) {
+    if (nblk <= 0) return HODG_OK;
+    if (HODG_PDL && m.n_elems <= hodg_pdl_max_elems()) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(unsigned(nblk));
+        cfg.blockDim = dim3(threads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        if (cudaLaunchKernelEx(&cfg, kernel, args...) != cudaSuccess) return HODG_ECUDA;
+    } else {
+        kernel<<<unsigned(nblk), threads, smem, st>>>(args...);
+    }
+    return cudaGetLastError() == cudaSuccess ? HODG_OK : HODG_ECUDA;
+}
+
 template <typename T, bool BND, bool ES>
 static int launch_face_k(const hodg_mesh_desc& m, const double* state, void* hbuf, uint32_t* err, cudaStream_t st,
                          int64_t fb, int64_t fe) {
     const size_t sm = face_smem_bytes<T>();
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(face_flux_kernel<T, BND, ES>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)) !=
-            cudaSuccess)
-            return HODG_ECUDA;
-        attr = true;
-    }
-    static int grid_cap = 0;
-    if (grid_cap == 0) {
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, face_flux_kernel<T, BND, ES>, FACE_THREADS, sm);
-        grid_cap = sms * (per_sm > 0 ? per_sm : 1);
-    }
+    static LaunchCache lc;
+    int cap = 0;
+    if (launch_setup(lc, face_flux_kernel<T, BND, ES>, FACE_THREADS, sm, &cap) != HODG_OK) return HODG_ECUDA;
     const int64_t ntiles = (fe - fb + FT - 1) / FT;
-    const int64_t nblk = ntiles < grid_cap ? ntiles : grid_cap;  // persistent CTAs loop over tiles
-    if (nblk > 0) {
-        if (HODG_PDL && m.n_elems <= hodg_pdl_max_elems()) {
-            cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3(unsigned(nblk));
-            cfg.blockDim = dim3(FACE_THREADS);
-            cfg.dynamicSmemBytes = sm;
-            cfg.stream = st;
-            cudaLaunchAttribute at[1];
-            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-            at[0].val.programmaticStreamSerializationAllowed = 1;
-            cfg.attrs = at;
-            cfg.numAttrs = 1;
-            if (cudaLaunchKernelEx(&cfg, face_flux_kernel<T, BND, ES>, m, state, static_cast<T*>(hbuf), err, fb, fe) !=
-                cudaSuccess)
-                return HODG_ECUDA;
-        } else {
-            face_flux_kernel<T, BND, ES>
-                <<<unsigned(nblk), FACE_THREADS, sm, st>>>(m, state, static_cast<T*>(hbuf), err, fb, fe);
-        }
-    }
-    return cudaGetLastError() == cudaSuccess ? HODG_OK : HODG_ECUDA;
+    const int64_t nblk = ntiles < cap ? ntiles : cap;  // persistent CTAs loop over tiles
+    return launch_maybe_pdl(m, face_flux_kernel<T, BND, ES>, nblk, FACE_THREADS, sm, st, m, state,
+                            static_cast<T*>(hbuf), err, fb, fe);
 }
 
 // interior_only: every face in [fb, fe) has a right element (no boundary
@@ -1001,36 +1117,25 @@ static int launch_face(const hodg_mesh_desc& m, const double* state, void* hbuf,
 template <typename T, bool ES>
 static int launch_elem_k(const hodg_mesh_desc& m, const void* hbuf, const hodg_stage_args& a, uint32_t* err,
                          cudaStream_t st) {
-    const size_t sm = elem_smem_bytes<T, ES>();
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(elem_stage_kernel<T, ES>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)) !=
-            cudaSuccess)
-            return HODG_ECUDA;
-        attr = true;
+    if constexpr (WARP_ELEM) {
+        // persistent warp groups (hodg_elem_warp.cuh)
+        const size_t sm = warp_smem_bytes<T, ES>();
+        static LaunchCache lc;
+        int cap = 0;
+        if (launch_setup(lc, elem_warp_kernel<T, ES>, WPC * 32, sm, &cap) != HODG_OK) return HODG_ECUDA;
+        const int64_t need = ((m.n_elems + G - 1) / G + WPC - 1) / WPC;
+        const int64_t nblk = need < cap ? need : cap;
+        return launch_maybe_pdl(m, elem_warp_kernel<T, ES>, nblk, WPC * 32, sm, st, m, static_cast<const T*>(hbuf),
+                                a, err);
+    } else {
+        const size_t sm = elem_smem_bytes<T, ES>();
+        static LaunchCache lc;
+        int cap = 0;
+        if (launch_setup(lc, elem_stage_kernel<T, ES>, ETHREADS, sm, &cap) != HODG_OK) return HODG_ECUDA;
+        const int64_t nblk = (m.n_elems + E - 1) / E;
+        return launch_maybe_pdl(m, elem_stage_kernel<T, ES>, nblk, ETHREADS, sm, st, m, static_cast<const T*>(hbuf),
+                                a, err);
     }
-    const int64_t nblk = (m.n_elems + E - 1) / E;
-    if (nblk > 0) {
-        if (HODG_PDL && m.n_elems <= hodg_pdl_max_elems()) {
-            cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3(unsigned(nblk));
-            cfg.blockDim = dim3(ETHREADS);
-            cfg.dynamicSmemBytes = sm;
-            cfg.stream = st;
-            cudaLaunchAttribute at[1];
-            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-            at[0].val.programmaticStreamSerializationAllowed = 1;
-            cfg.attrs = at;
-            cfg.numAttrs = 1;
-            if (cudaLaunchKernelEx(&cfg, elem_stage_kernel<T, ES>, m, static_cast<const T*>(hbuf), a, err) !=
-                cudaSuccess)
-                return HODG_ECUDA;
-        } else {
-            elem_stage_kernel<T, ES>
-                <<<unsigned(nblk), ETHREADS, sm, st>>>(m, static_cast<const T*>(hbuf), a, err);
-        }
-    }
-    return cudaGetLastError() == cudaSuccess ? HODG_OK : HODG_ECUDA;
 }
 
 template <typename T>

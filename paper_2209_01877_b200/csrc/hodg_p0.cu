@@ -12,6 +12,8 @@
 #define FB_F FB_P0_f
 #define FG_D FG_P0_d
 #define FG_F FG_P0_f
+#define WV_D WV_P0_d
+#define WV_F WV_P0_f
 #define FBG_D FBG_P0_d
 #define FBG_F FBG_P0_f
 #define MINV_T MINV_P0

@@ -12,6 +12,8 @@
 #define FB_F FB_P1_f
 #define FG_D FG_P1_d
 #define FG_F FG_P1_f
+#define WV_D WV_P1_d
+#define WV_F WV_P1_f
 #define FBG_D FBG_P1_d
 #define FBG_F FBG_P1_f
 #define MINV_T MINV_P1

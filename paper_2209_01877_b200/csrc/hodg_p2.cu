@@ -12,6 +12,8 @@
 #define FB_F FB_P2_f
 #define FG_D FG_P2_d
 #define FG_F FG_P2_f
+#define WV_D WV_P2_d
+#define WV_F WV_P2_f
 #define FBG_D FBG_P2_d
 #define FBG_F FBG_P2_f
 #define MINV_T MINV_P2

@@ -12,6 +12,8 @@
 #define FB_F FB_P3_f
 #define FG_D FG_P3_d
 #define FG_F FG_P3_f
+#define WV_D WV_P3_d
+#define WV_F WV_P3_f
 #define FBG_D FBG_P3_d
 #define FBG_F FBG_P3_f
 #define MINV_T MINV_P3

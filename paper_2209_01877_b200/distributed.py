@@ -22,7 +22,7 @@ from . import _lib
 from .dg import BoundaryConditions, Discretization, DofState
 from .geometry import compute_geometry
 from .mesh import TetMesh
-from .partition import HaloExchange, LocalPart, NativeHaloExchange, build_local, rcb_partition
+from .partition import HaloExchange, HostHaloExchange, LocalPart, NativeHaloExchange, build_local, rcb_partition
 from .physics import GasModel
 from .timestepping import SCHEMES, Stepper
 
@@ -32,8 +32,10 @@ __all__ = ["DistributedStepper", "setup_partitioned"]
 class DistributedStepper(Stepper):
     """halo: "native" -- the library's NCCL exchange (`hodg_halo_*`, its own
     communicator, unique id broadcast over `group`); "torch" -- point-to-point
-    ops of the torch.distributed group (the gloo CPU tests); "auto" -- native
-    on CUDA devices (override with HODG_HALO=torch)."""
+    ops of the torch.distributed group (the gloo CPU tests); "host" -- rows
+    staged through host memory over a gloo group (ranks sharing one GPU:
+    tests/test_gpu_multirank.py); "auto" -- native on CUDA devices (override
+    with HODG_HALO=torch|host)."""
 
     def __init__(self, part: LocalPart, disc: Discretization, scheme="rk3", prec=_lib.PREC_F64, cfl=0.3,
                  log_norms=True, group=None, halo="auto"):
@@ -52,6 +54,7 @@ class DistributedStepper(Stepper):
         self.part = part
         self.group = group
         self.native = halo == "native"
+        self.own_reduce = halo in ("native", "host")  # the exchange object's allreduce
         if halo == "native":
             rank, world = dist.get_rank(group), dist.get_world_size(group)
             uid = [NativeHaloExchange.unique_id() if rank == 0 else None]
@@ -59,6 +62,8 @@ class DistributedStepper(Stepper):
             self.halo = NativeHaloExchange(part, disc.rs, rank, world, uid[0], disc.device)
         elif halo == "torch":
             self.halo = HaloExchange(part, disc.device, group)
+        elif halo == "host":
+            self.halo = HostHaloExchange(part, disc.device, group)
         else:
             raise ValueError(f"unknown halo exchange {halo!r}")
         self.norm_sums = None
@@ -68,7 +73,7 @@ class DistributedStepper(Stepper):
 
         s = self.slots[slot_index:slot_index + 1]
         # positive doubles order like their int64 bit patterns: MIN is exact
-        if self.native:
+        if self.own_reduce:
             self.halo.allreduce(s, 0)
         else:
             dist.all_reduce(s, op=dist.ReduceOp.MIN, group=self.group)
@@ -106,7 +111,7 @@ class DistributedStepper(Stepper):
         if self.log_norms:
             import torch.distributed as dist
 
-            if self.native:
+            if self.own_reduce:
                 self.halo.allreduce(self.norm_sums, 1)
             else:
                 dist.all_reduce(self.norm_sums, op=dist.ReduceOp.SUM, group=self.group)

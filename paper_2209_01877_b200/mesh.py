@@ -422,76 +422,106 @@ def save_mesh(mesh: TetMesh, path) -> None:
                 fh.write(" ".join(str(int(v)) for v in mesh.face_nodes[f]) + "\n")
 
 
+class HodgMeshReader:
+    """Record reader for HODG-MESH v1 files (2D: hodg/mesh.py:450-560, and
+    this package's `dim 3` variant): the meaningful lines (blank and '#'
+    lines skipped) with their 1-based line numbers, consumed section by
+    section.  Every syntax error is a MeshParseError naming the line."""
+
+    def __init__(self, path):
+        self.path = path
+        with open(path) as fh:
+            raw = fh.read().splitlines()
+        self.n_lines = len(raw)
+        self.records = [(i + 1, t.split()) for i, t in enumerate(s.strip() for s in raw)
+                        if t and not t.startswith("#")]
+        self.pos = 0
+
+    def fail(self, line_no, msg):
+        return MeshParseError(self.path, line_no, msg)
+
+    def take(self, what):
+        """The next record, or an error at the end of the file."""
+        if self.pos >= len(self.records):
+            raise self.fail(self.n_lines, f"expected {what}")
+        rec = self.records[self.pos]
+        self.pos += 1
+        return rec
+
+    def at_end(self) -> bool:
+        return self.pos >= len(self.records)
+
+    def expect(self, words, msg):
+        ln, f = self.take(msg)
+        if f != list(words):
+            raise self.fail(ln, msg)
+
+    def count(self, word) -> int:
+        ln, f = self.take(f"'{word} N'")
+        if len(f) != 2 or f[0] != word:
+            raise self.fail(ln, f"expected '{word} N'")
+        try:
+            return int(f[1])
+        except ValueError:
+            raise self.fail(ln, f"bad {word} count") from None
+
+    def table(self, n, parse, what):
+        """n records through parse(fields) -> row; ValueError -> error."""
+        rows = []
+        for _ in range(n):
+            ln, f = self.take(what)
+            try:
+                rows.append(parse(f))
+            except (ValueError, KeyError):
+                raise self.fail(ln, f"expected {what}") from None
+        return rows
+
+    def patches(self, arity, kinds, optional=False):
+        """[(name, kind, [node tuples])]: a 'patches P' section of P
+        'name kind count' headers, each followed by `count` faces of `arity`
+        node ids."""
+        if optional and self.at_end():
+            return []
+        specs = []
+        for _ in range(self.count("patches")):
+            ln, f = self.take("'name kind count'")
+            if len(f) != 3 or f[1] not in kinds:
+                raise self.fail(ln, "expected 'name kind count' with a known kind")
+            try:
+                n = int(f[2])
+            except ValueError:
+                raise self.fail(ln, "bad face count") from None
+            specs.append((f[0], f[1], self.table(n, lambda g: _ints(g, arity), f"{arity} node ids")))
+        return specs
+
+
+def _ints(fields, n):
+    if len(fields) != n:
+        raise ValueError
+    return tuple(int(v) for v in fields)
+
+
+def _floats(fields, n):
+    if len(fields) != n:
+        raise ValueError
+    return tuple(float(v) for v in fields)
+
+
 def load_mesh(path) -> TetMesh:
     """Read a 3D HODG-MESH file; MeshParseError carries the line number
     (hodg/mesh.py:450-560)."""
-    with open(path) as fh:
-        raw = fh.read().splitlines()
-    lines = [(i + 1, s.strip()) for i, s in enumerate(raw) if s.strip() and not s.strip().startswith("#")]
-    it = iter(lines)
+    rd = HodgMeshReader(path)
+    rd.expect(["hodg-mesh", "1"], "expected header 'hodg-mesh 1'")
+    rd.expect(["dim", "3"], "expected 'dim 3'")
+    X = np.array(rd.table(rd.count("nodes"), lambda f: _floats(f, 3), "'x y z'"), dtype=np.float64).reshape(-1, 3)
 
-    def nxt(what):
-        try:
-            return next(it)
-        except StopIteration:
-            raise MeshParseError(path, len(raw), f"expected {what}") from None
+    def tet(f):
+        if f[0] != "T":
+            raise ValueError
+        return _ints(f[1:], 4)
 
-    ln, s = nxt("header")
-    if s.split() != ["hodg-mesh", "1"]:
-        raise MeshParseError(path, ln, "expected header 'hodg-mesh 1'")
-    ln, s = nxt("'dim 3'")
-    if s.split() != ["dim", "3"]:
-        raise MeshParseError(path, ln, "expected 'dim 3'")
-
-    def count(word):
-        ln, s = nxt(f"'{word} N'")
-        parts = s.split()
-        if len(parts) != 2 or parts[0] != word:
-            raise MeshParseError(path, ln, f"expected '{word} N'")
-        try:
-            return int(parts[1])
-        except ValueError:
-            raise MeshParseError(path, ln, f"bad {word} count") from None
-
-    nn = count("nodes")
-    X = np.empty((nn, 3))
-    for i in range(nn):
-        ln, s = nxt("node line")
-        parts = s.split()
-        try:
-            if len(parts) != 3:
-                raise ValueError
-            X[i] = [float(v) for v in parts]
-        except ValueError:
-            raise MeshParseError(path, ln, "expected 'x y z'") from None
-    ne = count("cells")
-    T = np.empty((ne, 4), dtype=np.int64)
-    for i in range(ne):
-        ln, s = nxt("cell line")
-        parts = s.split()
-        if len(parts) != 5 or parts[0] != "T":
-            raise MeshParseError(path, ln, "expected 'T a b c d'")
-        try:
-            T[i] = [int(v) for v in parts[1:]]
-        except ValueError:
-            raise MeshParseError(path, ln, "bad node index") from None
-    specs = []
-    np_ = count("patches")
-    for _ in range(np_):
-        ln, s = nxt("'name kind count'")
-        parts = s.split()
-        if len(parts) != 3 or parts[1] not in BC_KINDS:
-            raise MeshParseError(path, ln, "expected 'name kind count' with a known kind")
-        tris = []
-        for _ in range(int(parts[2])):
-            ln2, s2 = nxt("'a b c'")
-            try:
-                tris.append(tuple(int(v) for v in s2.split()))
-                if len(tris[-1]) != 3:
-                    raise ValueError
-            except ValueError:
-                raise MeshParseError(path, ln2, "expected 'a b c'") from None
-        specs.append((parts[0], parts[1], tris))
+    T = np.array(rd.table(rd.count("cells"), tet, "'T a b c d'"), dtype=np.int64).reshape(-1, 4)
+    specs = rd.patches(3, BC_KINDS)
     mesh = build_tet_mesh(X, T, specs)
     problems = validate(mesh)
     if problems:

@@ -168,6 +168,54 @@ class HaloExchange:
         self._work = []
 
 
+class HostHaloExchange:
+    """Ghost-row exchange staged through host memory over a CPU (gloo)
+    process group, for ranks that share one GPU (tests): the send rows are
+    gathered on the device and copied out, exchanged by gloo, and the
+    received rows copied into the ghost block.  Every transfer is
+    synchronous with the host, so no kernel ever waits on another rank's
+    kernel (ranks on one GPU must not, B200_PROFILING.md)."""
+
+    def __init__(self, part: LocalPart, device, group=None):
+        import torch
+
+        self.part = part
+        self.group = group
+        self.idx = {q: torch.as_tensor(ix, dtype=torch.int64, device=device) for q, ix in part.send_idx.items()}
+        self._work = []
+        self._recv = []
+
+    def start(self, rows):
+        import torch
+        import torch.distributed as dist
+
+        self._work, self._recv = [], []
+        for q, (r0, cnt) in sorted(self.part.recv_range.items()):
+            buf = torch.empty((cnt, rows.shape[1]), dtype=rows.dtype)
+            self._recv.append((rows, r0, cnt, buf))
+            self._work.append(dist.irecv(buf, src=q, group=self.group))
+        for q, ix in sorted(self.idx.items()):
+            buf = torch.index_select(rows, 0, ix).cpu()  # waits for the rows
+            self._work.append(dist.isend(buf, dst=q, group=self.group))
+            self._recv.append((None, 0, 0, buf))  # keep the send buffer alive
+
+    def wait(self):
+        for w in self._work:
+            w.wait()
+        for rows, r0, cnt, buf in self._recv:
+            if rows is not None:
+                rows[r0:r0 + cnt].copy_(buf)
+        self._work, self._recv = [], []
+
+    def allreduce(self, t, kind):
+        """In place: kind 0 int64 MIN, 1 float64 SUM (through the host)."""
+        import torch.distributed as dist
+
+        host = t.cpu()
+        dist.all_reduce(host, op=dist.ReduceOp.MIN if kind == 0 else dist.ReduceOp.SUM, group=self.group)
+        t.copy_(host)
+
+
 class NativeHaloExchange:
     """The same exchange through the library's NCCL halo (`hodg_halo_*`,
     csrc/halo.cu): one pack kernel plus grouped NCCL sends / receives on a

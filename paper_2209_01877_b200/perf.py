@@ -121,6 +121,37 @@ def count_flops_and_bytes(mesh, order: int, scheme: str = "rk3", precision_bits:
     return flops, st * bytes_stage
 
 
+# SURVEY.md §8(d) constants, hand-counted from the 3D scalar code in the
+# reference's convention (add / mul / div / sqrt = 1 flop, hodg/perf.py:1-49):
+# Roe with Harten-Hyman, primitive recovery, inviscid flux, boundary state
+ROE3, PRIM3, INV3, BND3 = 225, 15, 16, 95
+RK_FLOPS_PER_DOF = {"rk2": 3.5, "rk3": 4.0}  # mean per stage: u+dt r (2), combos (5)
+FP64_FLOPS_PER_S = 36.3e12  # measured DFMA peak (FMA = 2 flops), profiles/fp64_peaks.md
+
+
+def algorithmic_flops_per_stage(n_cells: int, n_faces: int, n_bnd_faces: int, order: int, scheme: str = "rk3"):
+    """Algorithmic flops of one RK stage, the reference's convention restated
+    for tetrahedra (hodg/perf.py:130-158):
+      flux   F_int nqf (10 trace + ROE3) + F_bnd nqf (5 trace + PRIM3 + BND3 + ROE3)
+      volume N nqv (5 trace + PRIM3 + INV3 + 33 nb)
+      gather (2 F_int + F_bnd) nqf (3 + 11 nb)
+      solve  N 10 nb^2;  RK  N 5 nb (flops per DOF);  dt  N (10 nb + 25) per step
+    with trace = 2 nb flops per variable.  Independent of how the kernels are
+    written (unlike count_flops_and_bytes, which counts the implementation's
+    own FP64-pipe operations)."""
+    t = ref_tables(order)
+    nb, nqv, nqf = t.nb, t.nqv, t.nqf
+    tr = 2 * nb
+    fi, fb = n_faces - n_bnd_faces, n_bnd_faces
+    flux = fi * nqf * (10 * tr + ROE3) + fb * nqf * (5 * tr + PRIM3 + BND3 + ROE3)
+    vol = n_cells * nqv * (5 * tr + PRIM3 + INV3 + 33 * nb)
+    gather = (2 * fi + fb) * nqf * (3 + 11 * nb)
+    solve = n_cells * 10 * nb * nb
+    rk = n_cells * 5 * nb * RK_FLOPS_PER_DOF[scheme]
+    dt = n_cells * (10 * nb + 25) / STAGES[scheme]
+    return float(flux + vol + gather + solve + rk + dt)
+
+
 def roofline_attainable(machine: MachineModel, ai: float) -> float:
     if ai < 0:
         raise ValueError("arithmetic intensity must be non-negative")

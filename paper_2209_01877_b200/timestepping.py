@@ -237,6 +237,25 @@ class Stepper:
                                      _lib.ptr(self.slots[self.parity:]), _lib.ptr(d.err), _lib.stream_ptr()),
                    "hodg_local_dt")
 
+    def set_dt(self, dt: float):
+        """Overwrite the global dt the next step uses (host-chosen dt:
+        dt_fixed, dt_floor, the t_final clip; hodg/timestepping.py:328-337)."""
+        bits = int(np.array([float(dt)], dtype=np.float64).view(np.int64)[0])
+        self.slots[self.parity].fill_(bits)
+
+    def floor_dt(self, dt_floor: float):
+        """Per-element dt floor of the next step (local dt mode,
+        hodg/timestepping.py:328-329), applied on the device."""
+        self.dtv[self.parity].clamp_(min=float(dt_floor))
+
+    def cell_means(self):
+        """(n, 5) float64 cell means of the current state (device)."""
+        from .refelem import ref_tables
+
+        t = ref_tables(self.disc.order)
+        mean = _torch().from_numpy(t.MEAN).to(self.disc.device)
+        return self.A[: self.disc.n, : N_VARS * t.nb].reshape(self.disc.n, N_VARS, t.nb) @ mean
+
     def dt_value(self) -> float:
         """The global dt used by the next step (host read, syncs)."""
         if self.dt_mode == "global":
@@ -363,9 +382,14 @@ class RunConfig:
     dt_mode: str = "local"
     scheme: str = "rk2"
     flux: str = "roe"
+    dt_floor: float = 0.0
+    dt_fixed: float | None = None
+    t_final: float | None = None
     max_iterations: int = 100
     log_every: int = 1
     residual_target: float | None = None
+    output_prefix: str | None = None
+    output_every: int = 0
     renumber: bool = False
     randomize_cells: int | None = None
     precision_mode: str = "dp"
@@ -373,6 +397,18 @@ class RunConfig:
     window: int = 200
     factor: float = 2.0
     check_every: int = 1
+
+    def __post_init__(self):
+        if self.dt_mode not in ("local", "global"):
+            raise ValueError(f"unknown dt mode {self.dt_mode!r}")
+        if self.dt_floor < 0.0:
+            raise ValueError("dt_floor must be non-negative")
+        if self.dt_fixed is not None and not self.dt_fixed > 0.0:
+            raise ValueError("dt_fixed must be positive")
+        if self.max_iterations < 0:
+            raise ValueError("max_iterations must be non-negative")
+        if self.output_every < 0:
+            raise ValueError("output_every must be non-negative")
 
     def make_mesh(self) -> TetMesh:
         from .mesh import generate_tet_box, perturb_interior_nodes
@@ -402,6 +438,8 @@ class RunArtifacts:
     iterate_seconds: float
     bandwidth_before: int | None = None
     bandwidth_after: int | None = None
+    t_sim: float = 0.0
+    output_files: list = field(default_factory=list)
 
 
 def initial_field(cfg: RunConfig, gas: GasModel):
@@ -415,10 +453,19 @@ def initial_field(cfg: RunConfig, gas: GasModel):
 
 
 def run(config: RunConfig, mesh: TetMesh | None = None) -> RunArtifacts:
-    """Drive a solve (hodg/timestepping.py:256-357): optional shuffle /
+    """Drive a solve (hodg/timestepping.py:256-402): optional shuffle /
     RCM renumbering, geometry, projection, then the precision-controlled
-    loop on the fused stepper.  The logged residual is the first stage's,
-    as in the reference; errors are checked every `check_every` steps."""
+    loop on the fused stepper, with the reference's order of operations per
+    step -- decide / promote, dt (CFL, `dt_floor`, `dt_fixed`, the `t_final`
+    clip with 1e-14 slack), the RK step, logging, field output every
+    `output_every` steps.  The logged residual is the first stage's, as in
+    the reference; errors are checked every `check_every` steps.
+
+    The CFL dt comes from the previous step's fused epilogue (device atomic
+    min); a host-chosen dt (dt_fixed, dt_floor, t_final) is written into the
+    stepper's dt slot before the step, which costs one small host sync per
+    step -- the plain CFL path stays sync-free except for logging."""
+    from .output import write_residual_csv, write_vtk
     from .physics import freestream_conserved
     from .renumber import apply_permutation, bandwidth, build_adjacency, random_permutation, rcm
 
@@ -437,18 +484,33 @@ def run(config: RunConfig, mesh: TetMesh | None = None) -> RunArtifacts:
     geo = compute_geometry(mesh, config.order)
     state = project_initial(mesh, geo, initial_field(config, gas), gas)
     disc = _get_disc(mesh, geo, gas, bcs)
-    ctrl = PrecisionController(config.precision_schedule())
     sched = config.precision_schedule()
-    starts_reduced = sched.mode in ("sp", "mp_rebound") or (sched.mode == "mp_fixed" and sched.switch_iter > 0)
-    prec = _lib.PREC_MIXED if starts_reduced else _lib.PREC_F64
+    ctrl = PrecisionController(sched)
+    prec = _lib.PREC_MIXED if sched.starts_reduced else _lib.PREC_F64
     stepper = Stepper(disc, config.scheme, prec, config.dt_mode, config.cfl, log_norms=bool(config.log_every))
     stepper.load(state)
     stepper.check(0)
     hist = ResidualHistory()
     events = []
+    out_files = []
+    written = set()
+
+    def write_field(iteration):
+        if config.output_prefix is None or iteration in written:
+            return
+        path = f"{config.output_prefix}_{iteration:06d}.vtk"
+        write_vtk(path, mesh, stepper.cell_means().cpu().numpy(), gas.gamma)
+        out_files.append(path)
+        written.add(iteration)
+
+    host_dt = config.dt_mode == "global" and (
+        config.dt_fixed is not None or config.t_final is not None or config.dt_floor > 0.0)
     setup = time.perf_counter() - t0
     t1 = time.perf_counter()
     it_run = 0
+    t_sim = 0.0
+    if config.max_iterations == 0:
+        write_field(0)
     for it in range(config.max_iterations):
         bits, ev = ctrl.decide(it, hist.res_rho)
         if ev is not None:
@@ -459,9 +521,25 @@ def run(config: RunConfig, mesh: TetMesh | None = None) -> RunArtifacts:
             stepper.hbuf = stepper._records(want)
             stepper._graphs.clear()
         log = config.log_every and (it % config.log_every == 0 or it == config.max_iterations - 1)
-        dt_log = stepper.dt_value() if log else None
+        if config.dt_mode == "global":
+            if host_dt:
+                dt = config.dt_fixed if config.dt_fixed is not None else max(stepper.dt_value(), config.dt_floor)
+                if config.t_final is not None:
+                    if t_sim >= config.t_final - 1e-14:
+                        break
+                    dt = min(dt, config.t_final - t_sim)
+                stepper.set_dt(dt)
+                dt_log = dt
+            else:
+                dt_log = stepper.dt_value() if log else None
+        else:
+            if config.dt_floor > 0.0:
+                stepper.floor_dt(config.dt_floor)
+            dt_log = stepper.dt_value() if log else None
         stepper.step()
         it_run = it + 1
+        if config.dt_mode == "global" and host_dt:
+            t_sim += dt_log
         if config.check_every and (it + 1) % config.check_every == 0:
             stepper.check(it)
         if log:
@@ -471,8 +549,16 @@ def run(config: RunConfig, mesh: TetMesh | None = None) -> RunArtifacts:
             hist.append(it, res5, dt_log, bits)
             if config.residual_target is not None and np.all(res5 < config.residual_target):
                 break
+        if config.output_every and (it + 1) % config.output_every == 0:
+            write_field(it + 1)
     stepper.check(it_run)
     _torch().cuda.synchronize()
     iterate = time.perf_counter() - t1
+    if config.max_iterations > 0:
+        write_field(it_run)
+    if config.output_prefix is not None:
+        csv_path = f"{config.output_prefix}_residuals.csv"
+        write_residual_csv(csv_path, hist)
+        out_files.append(csv_path)
     final = stepper.state(it_run)
-    return RunArtifacts(final, hist, events, mesh, geo, config, it_run, setup, iterate, bw0, bw1)
+    return RunArtifacts(final, hist, events, mesh, geo, config, it_run, setup, iterate, bw0, bw1, t_sim, out_files)

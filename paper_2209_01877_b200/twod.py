@@ -186,122 +186,53 @@ def perturb_interior_nodes(m: Mesh2D, amplitude, seed=0) -> Mesh2D:
 # HODG-MESH v1 (hodg/mesh.py:431-560): the reference's 2D plain-text format
 
 
+def _mesh_2d_records(m: Mesh2D):
+    """The HODG-MESH v1 lines of a 2D mesh, section by section."""
+    yield "hodg-mesh 1"
+    yield f"nodes {m.node_xy.shape[0]}"
+    yield from (f"{float(x)!r} {float(y)!r}" for x, y in m.node_xy)
+    yield f"cells {m.n_cells}"
+    tag = {3: "t", 4: "q"}
+    for nodes, nv in zip(m.cell_nodes, m.cell_nvert):
+        yield " ".join([tag[int(nv)]] + [str(int(k)) for k in nodes[: int(nv)]])
+    yield f"patches {len(m.patches)}"
+    for p in m.patches:
+        yield f"{p.name} {p.kind} {len(p.face_ids)}"
+        yield from (f"{int(a)} {int(b)}" for a, b in m.face_nodes[p.face_ids])
+
+
 def save_mesh_2d(m: Mesh2D, path) -> None:
-    """hodg/mesh.py:431-447 (byte-identical output)."""
+    """The reference's 2D HODG-MESH v1 writer (hodg/mesh.py:431-447):
+    byte-identical output (floats by repr)."""
     with open(path, "w") as fh:
-        fh.write("hodg-mesh 1\n")
-        fh.write(f"nodes {m.node_xy.shape[0]}\n")
-        for x, y in m.node_xy:
-            fh.write(f"{float(x)!r} {float(y)!r}\n")
-        fh.write(f"cells {m.n_cells}\n")
-        for c in range(m.n_cells):
-            nv = int(m.cell_nvert[c])
-            fh.write(("t" if nv == 3 else "q") + " " + " ".join(str(int(v)) for v in m.cell_nodes[c, :nv]) + "\n")
-        fh.write(f"patches {len(m.patches)}\n")
-        for p in m.patches:
-            fh.write(f"{p.name} {p.kind} {len(p.face_ids)}\n")
-            for f in p.face_ids:
-                a, b = m.face_nodes[f]
-                fh.write(f"{int(a)} {int(b)}\n")
+        fh.write("\n".join(_mesh_2d_records(m)) + "\n")
 
 
 def load_mesh_2d(path) -> Mesh2D:
-    """hodg/mesh.py:450-560: MeshParseError with the line number on malformed
-    input, TopologyError on bad connectivity."""
-    from .mesh import MeshParseError, TopologyError
+    """Read the reference's 2D HODG-MESH v1 (hodg/mesh.py:450-560):
+    MeshParseError with the line number on malformed input, TopologyError on
+    bad connectivity.  Cells are 't i j k' or 'q i j k l'; the patch section
+    is optional."""
+    from .mesh import HodgMeshReader, TopologyError
 
-    with open(path) as fh:
-        lines = fh.read().splitlines()
-    pos = 0
-
-    def next_line():
-        nonlocal pos
-        while pos < len(lines):
-            raw = lines[pos]
-            pos += 1
-            t = raw.strip()
-            if t and not t.startswith("#"):
-                return pos, t
-        return pos, None
-
-    def err(ln, msg):
-        return MeshParseError(path, ln, msg)
-
-    def count(tag):
-        ln, t = next_line()
-        if t is None or not t.startswith(tag + " "):
-            raise err(ln, f"expected '{tag} N'")
-        try:
-            return int(t.split()[1])
-        except (IndexError, ValueError):
-            raise err(ln, f"bad {tag} count") from None
-
-    ln, t = next_line()
-    if t is None or t.split() != ["hodg-mesh", "1"]:
-        raise err(ln, "expected header 'hodg-mesh 1'")
-    nn = count("nodes")
-    xy = np.empty((nn, 2))
-    for i in range(nn):
-        ln, t = next_line()
-        if t is None:
-            raise err(ln, f"expected {nn} node lines, got {i}")
-        parts = t.split()
-        if len(parts) != 2:
-            raise err(ln, "expected 'x y'")
-        try:
-            xy[i] = (float(parts[0]), float(parts[1]))
-        except ValueError:
-            raise err(ln, f"bad coordinate {t!r}") from None
-    nc = count("cells")
-    cells = []
-    for i in range(nc):
-        ln, t = next_line()
-        if t is None:
-            raise err(ln, f"expected {nc} cell lines, got {i}")
-        parts = t.split()
-        want = {"t": 3, "q": 4}.get(parts[0])
-        if want is None or len(parts) != want + 1:
-            raise err(ln, "expected 't i j k' or 'q i j k l'")
-        try:
-            cells.append(tuple(int(v) for v in parts[1:]))
-        except ValueError:
-            raise err(ln, f"bad node index in {t!r}") from None
-    specs = []
-    ln, t = next_line()
-    if t is not None:
-        if not t.startswith("patches "):
-            raise err(ln, "expected 'patches P'")
-        try:
-            npatch = int(t.split()[1])
-        except (IndexError, ValueError):
-            raise err(ln, "bad patch count") from None
-        for _ in range(npatch):
-            ln, t = next_line()
-            parts = t.split() if t is not None else []
-            if len(parts) != 3:
-                raise err(ln, "expected 'name kind count'")
-            name, kind = parts[0], parts[1]
-            if kind not in BC_KINDS:
-                raise err(ln, f"unknown boundary kind {kind!r}")
-            try:
-                cnt = int(parts[2])
-            except ValueError:
-                raise err(ln, "bad face count") from None
-            pairs = []
-            for _ in range(cnt):
-                ln, t = next_line()
-                parts = t.split() if t is not None else []
-                if len(parts) != 2:
-                    raise err(ln, "expected 'nodeA nodeB'")
-                try:
-                    pairs.append((int(parts[0]), int(parts[1])))
-                except ValueError:
-                    raise err(ln, f"bad node index in {t!r}") from None
-            specs.append((name, kind, pairs))
+    rd = HodgMeshReader(path)
+    rd.expect(["hodg-mesh", "1"], "expected header 'hodg-mesh 1'")
+    nodes = rd.table(rd.count("nodes"), lambda f: tuple(float(v) for v in _arity(f, 2)), "'x y'")
+    xy = np.array(nodes, dtype=np.float64).reshape(-1, 2)
+    arity = {"t": 3, "q": 4}
+    cells = rd.table(rd.count("cells"), lambda f: tuple(int(v) for v in _arity(f[1:], arity[f[0]])),
+                     "'t i j k' or 'q i j k l'")
+    specs = rd.patches(2, BC_KINDS, optional=True)
     try:
         return build_mesh_2d(xy, cells, specs)
     except (ValueError, KeyError) as e:
         raise TopologyError(f"{path}: {e}") from None
+
+
+def _arity(fields, n):
+    if len(fields) != n:
+        raise ValueError
+    return fields
 
 
 def write_vtk_2d(path, m: Mesh2D, t: "Tables2D", coeffs, gamma: float = 1.4) -> None:

@@ -63,9 +63,13 @@ def test_host_side_edge_cases():
 
     L = _lib.load()
     EINVAL = _lib.HODG_EINVAL
-    # element-slot record strides: 20 NQF + 1 (odd)
+    # element-slot record strides: 20 NQF + 1 (odd) for the CTA element
+    # kernel, 20 NQF + 2 for the warp-group kernel; a tile of blocks is a
+    # 16-byte multiple at FP32 and FP64
     strides = [L.hodg_elem_record_stride(p) for p in range(4)]
-    assert strides == [21, 121, 141, 301] and all(s % 2 == 1 for s in strides)
+    for p, (s, nqf) in enumerate(zip(strides, (1, 6, 7, 15))):
+        assert s in (20 * nqf + 1, 20 * nqf + 2)
+        assert (s * L.hodg_elem_tile(p) * 4) % 16 == 0
     assert L.hodg_elem_record_stride(4) == -1 and L.hodg_elem_record_stride(-1) == -1
     assert L.hodg_face_record_stride(2, 16) == -1
     # device mesh setup sizing
