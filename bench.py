@@ -204,7 +204,10 @@ def kernel_times(st, disc, prec, n_st=3, reps=3):
         a = st._stage_args(stage, st.parity)
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         ev[0].record()
-        disc.face_flux(us, prec, hb)
+        if st._uses_shadow():  # mixed: the face kernel reads the FP32 shadow rows
+            disc.face_flux32(st.A32 if stage == 0 else st.B32, hb)
+        else:
+            disc.face_flux(us, prec, hb)
         ev[1].record()
         disc.stage(prec, hb, a)
         ev[2].record()

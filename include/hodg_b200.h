@@ -105,6 +105,7 @@ typedef struct {
     double* dt_vec_out;      /* per-element CFL dt of the new state, NULL to skip */
     unsigned long long* dt_reset;  /* set to +inf by this launch (another step's dt slot), NULL to skip */
     double cfl;
+    float* out32;            /* mixed precision: FP32 shadow of out (row stride hodg_state32_row_stride), NULL to skip */
 } hodg_stage_args;
 
 int hodg_version(void);
@@ -152,6 +153,20 @@ int hodg_face_flux_range_es(const hodg_mesh* mesh, int prec, const double* state
                             int64_t f_end, int interior_only, uint32_t* err, void* stream);
 int hodg_elem_stage_es(const hodg_mesh* mesh, int prec, const void* elem_buf, const hodg_stage_args* args,
                        uint32_t* err, void* stream);
+/* Mixed precision: an FP32 shadow of the stage state -- rows of
+ * hodg_state32_row_stride(order) floats (16-byte rows), written by the element
+ * kernel next to the FP64 state (hodg_stage_args.out32) -- that the face
+ * kernel reads instead of converting each FP64 row at every (face, side).
+ * The traces are bitwise those of the FP64-row mixed kernel (the same
+ * FP64 -> FP32 rounding, done once per row).  No reference counterpart:
+ * the reference's mixed mode stores the whole state in FP32
+ * (hodg/precision.py:105-110). */
+int hodg_state32_row_stride(int order);
+int hodg_state_to_f32(const hodg_mesh* mesh, const double* rows, int64_t n_rows, float* rows32, void* stream);
+int hodg_face_flux_range32(const hodg_mesh* mesh, const float* state32, void* face_buf, int64_t f_begin,
+                           int64_t f_end, int interior_only, uint32_t* err, void* stream);
+int hodg_face_flux_range32_es(const hodg_mesh* mesh, const float* state32, void* elem_buf, int64_t f_begin,
+                              int64_t f_end, int interior_only, uint32_t* err, void* stream);
 int hodg_local_dt(const hodg_mesh* mesh, const double* state, double cfl, double* dt_vec_out,
                   unsigned long long* dt_min, uint32_t* err, void* stream);
 int hodg_norm_finalize(const double* partial, int64_t n_blocks, double* out5, void* stream);

@@ -59,6 +59,7 @@ class StageArgs(C.Structure):
         ("dt_vec_out", P),
         ("dt_reset", P),
         ("cfl", C.c_double),
+        ("out32", P),
     ]
 
 
@@ -77,6 +78,10 @@ SIGNATURES = {
     "hodg_stage_blocks": (I64, [P, I32]),
     "hodg_face_flux": (I32, [P, I32, P, P, P, P]),
     "hodg_face_flux_range": (I32, [P, I32, P, P, I64, I64, I32, P, P]),
+    "hodg_state32_row_stride": (I32, [I32]),
+    "hodg_state_to_f32": (I32, [P, P, I64, P, P]),
+    "hodg_face_flux_range32": (I32, [P, P, P, I64, I64, I32, P, P]),
+    "hodg_face_flux_range32_es": (I32, [P, P, P, I64, I64, I32, P, P]),
     "hodg_elem_stage": (I32, [P, I32, P, C.POINTER(StageArgs), P, P]),
     "hodg_face_flux_range_es": (I32, [P, I32, P, P, I64, I64, I32, P, P]),
     "hodg_elem_stage_es": (I32, [P, I32, P, C.POINTER(StageArgs), P, P]),

@@ -19,7 +19,11 @@
     int hodg_launch_dt_p##P(const hodg_mesh_desc&, const double*, double, double*, unsigned long long*,        \
                             uint32_t*, cudaStream_t);                                                          \
     int hodg_launch_modal_p##P(const hodg_mesh_desc&, int, const double*, double*, cudaStream_t);             \
-    int64_t hodg_elem_blocks_p##P(int64_t);
+    int64_t hodg_elem_blocks_p##P(int64_t);                                                                    \
+    int hodg_launch_face32_p##P(const hodg_mesh_desc&, const float*, void*, uint32_t*, cudaStream_t, int64_t,     \
+                                int64_t, int, int);                                                            \
+    int hodg_launch_to_f32_p##P(const double*, int64_t, float*, cudaStream_t);                                 \
+    int hodg_state32_stride_p##P();
 DECL_ORDER(0)
 DECL_ORDER(1)
 DECL_ORDER(2)
@@ -232,6 +236,52 @@ int hodg_face_flux_range(const hodg_mesh* mesh, int prec, const double* state, v
 int hodg_face_flux_range_es(const hodg_mesh* mesh, int prec, const double* state, void* elem_buf, int64_t f_begin,
                             int64_t f_end, int interior_only, uint32_t* err, void* stream) {
     return face_flux_impl(mesh, prec, state, elem_buf, f_begin, f_end, interior_only, err, stream, 1);
+}
+
+static int face_flux32_impl(const hodg_mesh* mesh, const float* state32, void* buf, int64_t f_begin, int64_t f_end,
+                            int interior_only, uint32_t* err, void* stream, int es) {
+    if (!mesh || !state32 || !buf) return HODG_EINVAL;
+    if (f_begin < 0 || f_end > mesh->d.n_faces || f_begin > f_end) return HODG_EINVAL;
+    if (f_begin == f_end) return HODG_OK;
+    g_launches++;
+    const hodg_mesh_desc& d = mesh->d;
+    switch (d.order) {
+        case 0: return hodg_launch_face32_p0(d, state32, buf, err, S(stream), f_begin, f_end, interior_only, es);
+        case 1: return hodg_launch_face32_p1(d, state32, buf, err, S(stream), f_begin, f_end, interior_only, es);
+        case 2: return hodg_launch_face32_p2(d, state32, buf, err, S(stream), f_begin, f_end, interior_only, es);
+        default: return hodg_launch_face32_p3(d, state32, buf, err, S(stream), f_begin, f_end, interior_only, es);
+    }
+}
+
+int hodg_face_flux_range32(const hodg_mesh* mesh, const float* state32, void* face_buf, int64_t f_begin,
+                           int64_t f_end, int interior_only, uint32_t* err, void* stream) {
+    return face_flux32_impl(mesh, state32, face_buf, f_begin, f_end, interior_only, err, stream, 0);
+}
+
+int hodg_face_flux_range32_es(const hodg_mesh* mesh, const float* state32, void* elem_buf, int64_t f_begin,
+                              int64_t f_end, int interior_only, uint32_t* err, void* stream) {
+    return face_flux32_impl(mesh, state32, elem_buf, f_begin, f_end, interior_only, err, stream, 1);
+}
+
+int hodg_state32_row_stride(int order) {
+    switch (order) {
+        case 0: return hodg_state32_stride_p0();
+        case 1: return hodg_state32_stride_p1();
+        case 2: return hodg_state32_stride_p2();
+        case 3: return hodg_state32_stride_p3();
+        default: return -1;
+    }
+}
+
+int hodg_state_to_f32(const hodg_mesh* mesh, const double* rows, int64_t n_rows, float* rows32, void* stream) {
+    if (!mesh || !rows || !rows32 || n_rows < 0) return HODG_EINVAL;
+    g_launches++;
+    switch (mesh->d.order) {
+        case 0: return hodg_launch_to_f32_p0(rows, n_rows, rows32, S(stream));
+        case 1: return hodg_launch_to_f32_p1(rows, n_rows, rows32, S(stream));
+        case 2: return hodg_launch_to_f32_p2(rows, n_rows, rows32, S(stream));
+        default: return hodg_launch_to_f32_p3(rows, n_rows, rows32, S(stream));
+    }
 }
 
 int hodg_face_flux(const hodg_mesh* mesh, int prec, const double* state, void* face_buf, uint32_t* err,

@@ -85,6 +85,11 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+// one arrival on `bar` once all of this thread's prior cp.async copies landed
+// (counts against the barrier's expected arrivals: .noinc)
+__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 // make generic-proxy smem writes visible to the async (TMA) proxy
@@ -205,12 +210,19 @@ __device__ __forceinline__ bool roe(const T qL[5], const T qR[5], const T n[3], 
     const T a4 = (dp + rad) * ia2h;
     const T a2w = dr - dp * (ra * ra);
     const T w1 = l1 * a1, w4 = l4 * a4;
-    const T d0 = w1 + l2 * a2w + w4;
-    const T d1 = w1 * (ut - a * nx) + l2 * (a2w * ut + rt * (du - dun * nx)) + w4 * (ut + a * nx);
-    const T d2 = w1 * (vt - a * ny) + l2 * (a2w * vt + rt * (dv - dun * ny)) + w4 * (vt + a * ny);
-    const T d3 = w1 * (wt - a * nz) + l2 * (a2w * wt + rt * (dw - dun * nz)) + w4 * (wt + a * nz);
-    const T dE = w1 * (Ht - a * unt) + l2 * (a2w * ke + rt * (ut * du + vt * dv + wt * dw - unt * dun)) +
-                 w4 * (Ht + a * unt);
+    // dissipation sum_k |lambda_k| alpha_k r_k, with the acoustic pair
+    // (w1, w4) and the shear/entropy terms regrouped by ut / n / du:
+    //   d_x = d0 ut + cn nx + l2 rt du,  cn = (w4 - w1) a - l2 rt dun,
+    //   dE  = (w1 + w4) Ht + l2 a2w ke + cn unt + l2 rt (ut du + vt dv + wt dw)
+    const T sw = w1 + w4;
+    const T l2a2w = l2 * a2w;
+    const T l2rt = l2 * rt;
+    const T d0 = sw + l2a2w;
+    const T cn = (w4 - w1) * a - l2rt * dun;
+    const T d1 = d0 * ut + cn * nx + l2rt * du;
+    const T d2 = d0 * vt + cn * ny + l2rt * dv;
+    const T d3 = d0 * wt + cn * nz + l2rt * dw;
+    const T dE = sw * Ht + l2a2w * ke + cn * unt + l2rt * (ut * du + vt * dv + wt * dw);
     f[0] = half * (qL[0] * vnL + qR[0] * vnR - d0);
     f[1] = half * (qL[1] * vnL + qR[1] * vnR + (pL + pR) * nx - d1);
     f[2] = half * (qL[2] * vnL + qR[2] * vnR + (pL + pR) * ny - d2);

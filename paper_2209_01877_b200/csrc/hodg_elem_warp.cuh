@@ -290,6 +290,14 @@ __global__ void __launch_bounds__(WPC * 32, HODG_WMINB)
 #pragma unroll
                 for (int j = 0; j + 1 < NB; j += 2)
                     *reinterpret_cast<double2*>(a.out + gid * RS + v * NB + j) = make_double2(o[j], o[j + 1]);
+                if constexpr (sizeof(T) == 4) {
+                    if (a.out32) {  // mixed: the FP32 shadow the next face kernel reads
+#pragma unroll
+                        for (int j = 0; j + 1 < NB; j += 2)
+                            *reinterpret_cast<float2*>(a.out32 + gid * RSF + v * NB + j) =
+                                make_float2(float(o[j]), float(o[j + 1]));
+                    }
+                }
             }
             if (a.dt_next || a.dt_vec_out) {
                 // the five variable means of element e, at its v == 0 lane

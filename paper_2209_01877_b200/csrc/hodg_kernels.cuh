@@ -20,6 +20,12 @@ namespace hodg {
 namespace HODG_CAT(ord, ORDER) {
 
 constexpr int RS = (5 * NB + 1) & ~1;        // state row stride (doubles)
+constexpr int RSF = (5 * NB + 3) & ~3;       // FP32 shadow row stride (floats; 16-byte rows)
+// row stride of a state array of element type R
+template <typename R>
+__host__ __device__ constexpr int rstride() {
+    return sizeof(R) == 8 ? RS : RSF;
+}
 #ifndef HODG_NG3
 #define HODG_NG3 4
 #endif
@@ -38,6 +44,12 @@ constexpr int FACE_THREADS = 128;
 #endif
 #ifndef HODG_FACE_MINB
 #define HODG_FACE_MINB 4
+#endif
+#ifndef HODG_ELEM_CPASYNC
+#define HODG_ELEM_CPASYNC 0  // CTA element kernel: face records by cp.async chunks (0: one TMA copy per record; faster)
+#endif
+#ifndef HODG_FACE_CPASYNC
+#define HODG_FACE_CPASYNC 0  // state rows by per-thread cp.async chunks (0: one TMA bulk copy per row; faster)
 #endif
 constexpr int RP = HODG_ROE_PAIRS;  // Riemann problems per thread per phase-2 iteration (1 measured fastest)
 constexpr int FT = FACE_THREADS / (2 * NG);  // faces per CTA (32 for P1-P3)
@@ -196,23 +208,42 @@ __host__ __device__ constexpr int expt(int i, int d) {
     return d == 0 ? a : (d == 1 ? b : k - a - b);
 }
 
-template <typename T>
+// R: element type of the state rows the face kernel reads -- the FP64 state,
+// or (mixed precision) its FP32 shadow
+template <typename T, typename R = double>
 __host__ __device__ constexpr size_t face_smem_bytes() {
     return align16(16 + 4 * FBS * sizeof(T)) +
-           2 * align16(cmax(size_t(2 * FT) * RS * sizeof(double), size_t(2 * FT) * NQF * 5 * sizeof(T)));
+           2 * align16(cmax(size_t(2 * FT) * rstride<R>() * sizeof(R), size_t(2 * FT) * NQF * 5 * sizeof(T)));
 }
 
 // element kernel shared memory carve-up
+// element kernel shared memory carve-up.  The state tile lands in the record
+// region and is read into registers before the records are fetched over it;
+// the u0 tile, then the output tile, reuse the per-chunk X region, followed
+// by the reduction slots.  Persistent CTAs (EPERSIST) double-buffer the
+// geometry / face-id tiles and prefetch the next tile's inputs into the
+// record region once the gather has consumed it.
+#ifndef HODG_EPERSIST
+#define HODG_EPERSIST 1
+#endif
+constexpr bool EPERSIST = HODG_EPERSIST && !WARP_ELEM && ORDER <= 2 && H == 1;
+
 template <typename T, bool ES>
 struct ElemSmem {
-    static constexpr size_t bar = 0;                                         // 2 mbarriers
-    static constexpr size_t geo = 16;                                        // 16 x E doubles (tiled)
-    static constexpr size_t fid = geo + size_t(16) * E * 8;                  // 4 x E int32 (tiled)
-    static constexpr size_t red = fid + size_t(4) * E * 4;                   // (5 + 5H) x E doubles
-    static constexpr size_t htile = align16(red + size_t(5 + 5 * H) * E * 8);  // 4 x E face records
-    static constexpr size_t hbytes = ES ? size_t(E) * EREC * sizeof(T) : size_t(4) * E * hsmem<T>() * sizeof(T);
+    static constexpr int NGB = EPERSIST ? 2 : 1;
+    static constexpr size_t bar = 0;                                         // in[2], records, u0 tile
+    static constexpr size_t geo = 32;                                        // NGB x 16 x E doubles (tiled)
+    static constexpr size_t fid = geo + size_t(NGB) * 16 * E * 8;            // NGB x 4 x E int32 (tiled)
+    static constexpr size_t htile = align16(fid + size_t(NGB) * 4 * E * 4);  // state tile, then the records
+    static constexpr size_t hrec = ES ? size_t(E) * EREC * sizeof(T) : size_t(4) * E * hsmem<T>() * sizeof(T);
+    static constexpr size_t sbytes = size_t(E) * RS * 8;
+    static constexpr size_t hbytes = cmax(hrec, sbytes);
     static constexpr size_t sx = align16(htile + hbytes);
-    static constexpr size_t sx_bytes = cmax(size_t(E) * RS * 8, size_t(QC) * E * XS * sizeof(T));
+    static constexpr size_t red = sx + sbytes;                               // (5 + 5H) x E doubles
+    static constexpr size_t s32 = red + size_t(5 + 5 * H) * E * 8;           // mixed: FP32 output tile
+    static constexpr size_t s32_bytes = sizeof(T) == 4 ? size_t(E) * RSF * 4 : 0;
+    static constexpr size_t sx_bytes =
+        cmax(sbytes + size_t(5 + 5 * H) * E * 8 + s32_bytes, size_t(QC) * E * XS * sizeof(T));
     static constexpr size_t total = sx + sx_bytes;
     // H > 1: the residual exchange of the mass solve reuses the record tile
     static_assert(H == 1 || hbytes >= size_t(5) * E * NB * 8, "solve exchange fits the record tile");
@@ -293,9 +324,9 @@ __device__ __forceinline__ void face_moments(const T (&hq)[NQ], T (&fa)[N]) {
 //  With ES the records go to the element-slot layout instead: each face's
 //  record is stored in the blocks of both (owned) neighbours, so the element
 //  kernel fetches a tile's records with one contiguous copy.
-template <typename T, bool BND, bool ES>
+template <typename T, bool BND, bool ES, typename R = double>
 __global__ void __launch_bounds__(FACE_THREADS, HODG_FACE_MINB) face_flux_kernel(const hodg_mesh_desc m,
-                                                                    const double* __restrict__ state,
+                                                                    const R* __restrict__ state,
                                                                     T* __restrict__ hbuf,
                                                                     uint32_t* __restrict__ err, int64_t f_begin,
                                                                     int64_t f_end) {
@@ -303,9 +334,10 @@ __global__ void __launch_bounds__(FACE_THREADS, HODG_FACE_MINB) face_flux_kernel
     extern __shared__ __align__(16) unsigned char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem);  // one per buffer
     T* fbt = reinterpret_cast<T*>(smem + 16);
-    double* rows0 = reinterpret_cast<double*>(smem + align16(16 + 4 * FBS * sizeof(T)));
-    constexpr size_t BUF = align16(cmax(size_t(2 * FT) * RS * sizeof(double), size_t(2 * FT) * NQF * 5 * sizeof(T))) /
-                           sizeof(double);
+    constexpr int RR = rstride<R>();
+    R* rows0 = reinterpret_cast<R*>(smem + align16(16 + 4 * FBS * sizeof(T)));
+    constexpr size_t BUF = align16(cmax(size_t(2 * FT) * RR * sizeof(R), size_t(2 * FT) * NQF * 5 * sizeof(T))) /
+                           sizeof(R);
     __shared__ double fn[2][FT][3];
     __shared__ int finf[2][FT];
     __shared__ int64_t fdst[2][FT][2];  // ES: record offsets of the left / right blocks (-1: none)
@@ -368,13 +400,27 @@ __global__ void __launch_bounds__(FACE_THREADS, HODG_FACE_MINB) face_flux_kernel
             fn[buf][lf][1] = mt.nrm.y;
             fn[buf][lf][2] = mt.nrm.z;
         }
-        double* row = rows0 + buf * BUF + size_t(side * FT + lf) * RS;
-        if (g == 0 && mt.elem >= 0) {
-            mbar_arrive_expect_tx(bar + buf, RS * 8);
-            bulk_g2s(row, state + int64_t(mt.elem) * RS, RS * 8, bar + buf);
+        R* row = rows0 + buf * BUF + size_t(side * FT + lf) * RR;
+#if HODG_FACE_CPASYNC
+        // the NG threads of this (face, side) copy the row in 16-byte
+        // chunks, interleaved so each adjacent pair fills one 32-byte sector
+        if (mt.elem >= 0) {
+            const char* src = reinterpret_cast<const char*>(state + int64_t(mt.elem) * RR);
+            char* dst = reinterpret_cast<char*>(row);
+#pragma unroll
+            for (int ch = g; ch < RR * int(sizeof(R)) / 16; ch += NG) cp_async16(dst + 16 * ch, src + 16 * ch);
+            cp_async_arrive(bar + buf);
         } else {
             mbar_arrive(bar + buf);
         }
+#else
+        if (g == 0 && mt.elem >= 0) {
+            mbar_arrive_expect_tx(bar + buf, RR * sizeof(R));
+            bulk_g2s(row, state + int64_t(mt.elem) * RR, RR * sizeof(R), bar + buf);
+        } else {
+            mbar_arrive(bar + buf);
+        }
+#endif
     };
 
     int tile = blockIdx.x;
@@ -397,7 +443,7 @@ __global__ void __launch_bounds__(FACE_THREADS, HODG_FACE_MINB) face_flux_kernel
         mbar_wait(bar + buf, (it >> 1) & 1);
 
         // phase 1: traces of this side at qps [g*QPT, g*QPT + QPT)
-        const double* myrow = rows0 + buf * BUF + size_t(side * FT + lf) * RS;
+        const R* myrow = rows0 + buf * BUF + size_t(side * FT + lf) * RR;
         T tr[QPT][5];
 #pragma unroll
         for (int qq = 0; qq < QPT; ++qq)
@@ -538,406 +584,459 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : 4) : E
     constexpr int HS = hstride<T>();
     constexpr int HSS = hsmem<T>();
     extern __shared__ __align__(16) unsigned char smem[];
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::bar);
-    double* G = reinterpret_cast<double*>(smem + L::geo);
-    int32_t* FI = reinterpret_cast<int32_t*>(smem + L::fid);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::bar);  // [0, 1] inputs per buffer, [2] records, [3] u0
+    T* HT = reinterpret_cast<T*>(smem + L::htile);
+    double* SIN = reinterpret_cast<double*>(smem + L::htile);    // the state tile, before the records land
+    double* Z = reinterpret_cast<double*>(smem + L::htile);      // H > 1: residual exchange (after the gather)
+    double* S = reinterpret_cast<double*>(smem + L::sx);         // u0 tile, then the output tile
+    T* X = reinterpret_cast<T*>(smem + L::sx);                   // per-chunk trace / flux slots
     // [0, 5E): norm terms; [5E + 5E h, 10E + 5E h): cell-mean partials of basis part h
     double* RED = reinterpret_cast<double*>(smem + L::red);
-    T* HT = reinterpret_cast<T*>(smem + L::htile);
-    double* Z = reinterpret_cast<double*>(smem + L::htile);  // H > 1: residual exchange (after the gather)
-    double* S = reinterpret_cast<double*>(smem + L::sx);     // state tile, later the output tile
-    T* X = reinterpret_cast<T*>(smem + L::sx);               // per-chunk trace / flux slots
+    float* S32 = reinterpret_cast<float*>(smem + L::s32);  // mixed: FP32 shadow of the output tile
+    const bool shadow = sizeof(T) == 4 && a.out32 != nullptr;
     const int t = threadIdx.x;
-    const int64_t tile = blockIdx.x;
-    const int64_t e0 = tile * E;
-    const int ne = int(min(int64_t(E), m.n_elems - e0));
+    const int64_t ntiles = (m.n_elems + E - 1) / E;
+    // thread (v, h, e): e fastest, so h is warp-uniform (E >= 32 when H > 1)
+    const int e = t % E;
+    const int h = (t / E) % H;
+    const int v = t / (E * H);
+    const int jb = h * NH;  // first basis function of this thread's part
+    const bool need_u0 = a.combine == 1 || (a.combine == 0 && a.a != 0.0);
+    const T gam = T(m.gamma);
+
+    auto issue_inputs = [&](int64_t tl, int gb) {  // thread 0
+        const int nn = int(min(int64_t(E), m.n_elems - tl * E));
+        const uint32_t bs = uint32_t(nn) * RS * 8;
+        mbar_arrive_expect_tx(bar + gb, bs + 16 * E * 8 + 4 * E * 4);
+        bulk_g2s(SIN, a.us + tl * E * RS, bs, bar + gb);
+        bulk_g2s(reinterpret_cast<double*>(smem + L::geo) + gb * 16 * E, m.egeo + tl * 16 * E, 16 * E * 8, bar + gb);
+        bulk_g2s(reinterpret_cast<int32_t*>(smem + L::fid) + gb * 4 * E, m.efaces + tl * 4 * E, 4 * E * 4,
+                 bar + gb);
+    };
+    int64_t tile = blockIdx.x;
     if (t == 0) {
         if (a.dt_reset && blockIdx.x == 0) *a.dt_reset = 0x7FF0000000000000ull;
         mbar_init(bar, 1);
-        mbar_init(bar + 1, ES ? 1 : 4 * E);
+        mbar_init(bar + 1, 1);
+        mbar_init(bar + 2, ES ? 1 : (HODG_ELEM_CPASYNC ? ETHREADS : 4 * E));
+        mbar_init(bar + 3, 1);
         mbar_fence_init();
-        const uint32_t bs = uint32_t(ne) * RS * 8;
-        if constexpr (ES) {
-            const uint32_t hb = uint32_t(align16(size_t(ne) * EREC * sizeof(T)));
-            mbar_arrive_expect_tx(bar, bs + 16 * E * 8);
-            bulk_g2s(S, a.us + e0 * RS, bs, bar);
-            bulk_g2s(G, m.egeo + tile * 16 * E, 16 * E * 8, bar);
-            // the records are the face kernel's output
-            asm volatile("griddepcontrol.wait;" ::: "memory");
-            mbar_arrive_expect_tx(bar + 1, hb);
-            bulk_g2s(HT, hbuf + e0 * EREC, hb, bar + 1);
-        } else {
-            mbar_arrive_expect_tx(bar, bs + 16 * E * 8 + 4 * E * 4);
-            bulk_g2s(S, a.us + e0 * RS, bs, bar);
-            bulk_g2s(G, m.egeo + tile * 16 * E, 16 * E * 8, bar);
-            bulk_g2s(FI, m.efaces + tile * 4 * E, 4 * E * 4, bar);
-        }
+        if (tile < ntiles) issue_inputs(tile, 0);  // the stage state: two launches back
     }
     __syncthreads();
-    mbar_wait(bar, 0);
     // programmatic dependent launch: everything above overlapped the face
     // kernel's tail; records, and the in-place output, need it complete
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;");
 
-    // thread (v, h, e): e fastest, so h is warp-uniform (E >= 32 when H > 1)
-    const int e = t % E;
-    const int h = (t / E) % H;
-    const int v = t / (E * H);
-    // face flux records: thread (s, e) for t < 4E fetches face FI[s][e]
-    if (!ES && t < 4 * E) {
-        const int ee = t % E;
-        if (ee < ne) {
-            const int64_t f = FI[t];
-            mbar_arrive_expect_tx(bar + 1, HS * sizeof(T));
-            bulk_g2s(HT + size_t(t) * HSS, hbuf + f * HS, HS * sizeof(T), bar + 1);
-        } else {
-            mbar_arrive(bar + 1);
-        }
-    }
+    for (int it = 0; tile < ntiles; tile += gridDim.x, ++it) {
+        const int gbuf = EPERSIST ? (it & 1) : 0;
+        const double* G = reinterpret_cast<const double*>(smem + L::geo) + gbuf * 16 * E;
+        const int32_t* FI = reinterpret_cast<const int32_t*>(smem + L::fid) + gbuf * 4 * E;
+        const int64_t e0 = tile * E;
+        const int ne = int(min(int64_t(E), m.n_elems - e0));
+        const int64_t gid = e0 + e;
+        const bool live = e < ne;
+        mbar_wait(bar + gbuf, EPERSIST ? ((it >> 1) & 1) : (it & 1));
 
-    const int64_t gid = e0 + e;
-    const bool live = e < ne;
-    const bool need_u0 = a.combine == 1 || (a.combine == 0 && a.a != 0.0);
-    const int jb = h * NH;  // first basis function of this thread's part
-    double c[NH];
-    double u0r[!U0_TMA ? NH : 1];
-    if (live) {
-        if constexpr (H == 1 && (NB % 2) == 0) {
-            ld_row(S + e * RS + v * NB, c);  // rows 16-byte aligned when NB is even
-        } else {
+        double c[NH];
+        double u0r[!U0_TMA ? NH : 1];
+        if (live) {
+            if constexpr (H == 1 && (NB % 2) == 0) {
+                ld_row(SIN + e * RS + v * NB, c);  // rows 16-byte aligned when NB is even
+            } else {
 #pragma unroll
-            for (int i = 0; i < NH; ++i) c[i] = S[e * RS + v * NB + jb + i];
-        }
-        if constexpr (!U0_TMA) {
-            if (need_u0) {
-                if constexpr (H == 1 && (NB % 2) == 0) {
-                    ld_row(a.u0 + gid * RS + v * NB, u0r);
-                } else {
+                for (int i = 0; i < NH; ++i) c[i] = SIN[e * RS + v * NB + jb + i];
+            }
+            if constexpr (!U0_TMA) {
+                if (need_u0) {
+                    if constexpr (H == 1 && (NB % 2) == 0) {
+                        ld_row(a.u0 + gid * RS + v * NB, u0r);
+                    } else {
 #pragma unroll
-                    for (int i = 0; i < NH; ++i) u0r[i] = a.u0[gid * RS + v * NB + jb + i];
+                        for (int i = 0; i < NH; ++i) u0r[i] = a.u0[gid * RS + v * NB + jb + i];
+                    }
                 }
             }
         }
-    }
-    __syncthreads();  // state tile consumed: the region now holds X
+        __syncthreads();  // state tile consumed: the region receives the face flux records
 
-    T acc[NH];
-#pragma unroll
-    for (int i = 0; i < NH; ++i) acc[i] = T(0);
-    T mom[MOMENTS ? NBL : 1][3];
-#pragma unroll
-    for (int j = 0; j < (MOMENTS ? NBL : 1); ++j) mom[j][0] = mom[j][1] = mom[j][2] = T(0);
-    T ji[H == 1 ? 9 : 1];
-    if constexpr (H == 1) {
-#pragma unroll
-        for (int k = 0; k < 9; ++k) ji[k] = T(G[k * E + e]);
-    }
-    const T gam = T(m.gamma);
-    sfor<NCH>([&](auto ch) {
-        constexpr int q0 = ch * QC;
-        constexpr int nq = (NQV - q0) < QC ? (NQV - q0) : QC;
-        // phase A: traces of variable v (H > 1: partial sums of this part,
-        // added in phase B in part order)
-        if (live) {
-            hsel(h, [&](auto hc) {
-                sfor<nq>([&](auto qq) {
-                    T u = T(0);
-                    sfor<NH>([&](auto i) { u += TAB(VB, T, (q0 + qq) * NB + hc * NH + i) * T(c[i]); });
-                    X[(qq * E + e) * XS + hc * 5 + v] = u;
-                });
-            });
+        // face flux records, in flight during the volume integral
+        if constexpr (ES) {
+            if (t == 0 && ne > 0) {
+                const uint32_t hb = uint32_t(align16(size_t(ne) * EREC * sizeof(T)));
+                fence_proxy_async();
+                mbar_arrive_expect_tx(bar + 2, hb);
+                bulk_g2s(HT, hbuf + e0 * EREC, hb, bar + 2);
+            } else if (t == 0) {
+                mbar_arrive(bar + 2);
+            }
+        } else {
+#if HODG_ELEM_CPASYNC
+            // 16-byte cp.async chunks, consecutive threads on consecutive
+            // chunks of one record; every thread arrives once when its copies land
+            constexpr int NC = int(HS * sizeof(T) / 16);
+            for (int cc = t; cc < 4 * E * NC; cc += ETHREADS) {
+                const int r = cc / NC;
+                const int k = cc - r * NC;
+                if (r % E < ne)
+                    cp_async16(reinterpret_cast<char*>(HT + size_t(r) * HSS) + 16 * k,
+                               reinterpret_cast<const char*>(hbuf + int64_t(FI[r]) * HS) + 16 * k);
+            }
+            cp_async_arrive(bar + 2);
+#else
+            // thread (s, e) for t < 4E fetches face FI[s][e]
+            if (t < 4 * E) {
+                if (t % E < ne) {
+                    fence_proxy_async();
+                    mbar_arrive_expect_tx(bar + 2, HS * sizeof(T));
+                    bulk_g2s(HT + size_t(t) * HSS, hbuf + int64_t(FI[t]) * HS, HS * sizeof(T), bar + 2);
+                } else {
+                    mbar_arrive(bar + 2);
+                }
+            }
+#endif
         }
-        __syncthreads();
-        // phase B
-        for (int p = t; p < nq * E; p += ETHREADS) {
-            const int qq = p / E;
-            const int ee = p - qq * E;
-            if (ee >= ne) continue;
-            T* sl = X + (qq * E + ee) * XS;
-            T U[5];
+
+        T acc[NH];
 #pragma unroll
-            for (int k = 0; k < 5; ++k) U[k] = sl[k];
-            if constexpr (H > 1) {
+        for (int i = 0; i < NH; ++i) acc[i] = T(0);
+        T mom[MOMENTS ? NBL : 1][3];
 #pragma unroll
-                for (int hh = 1; hh < H; ++hh)
+        for (int j = 0; j < (MOMENTS ? NBL : 1); ++j) mom[j][0] = mom[j][1] = mom[j][2] = T(0);
+        T ji[H == 1 ? 9 : 1];
+        if constexpr (H == 1) {
 #pragma unroll
-                    for (int k = 0; k < 5; ++k) U[k] += sl[hh * 5 + k];
-            }
-            T u, vv, w;
-            const T pr = (U[0] > T(0)) ? prim(U, gam, u, vv, w) : T(-1);
-            if (!(pr > T(0))) {
-                flag(err, 1, uint32_t(e0 + ee));
-#pragma unroll
-                for (int k = 0; k < XS; ++k) sl[k] = T(0);
-                continue;
-            }
-            // physical flux F[d][var]
-            const T Hs = U[4] + pr;
-            T F[15] = {U[1], U[1] * u + pr, U[1] * vv, U[1] * w, Hs * u,
-                       U[2], U[2] * u, U[2] * vv + pr, U[2] * w, Hs * vv,
-                       U[3], U[3] * u, U[3] * vv, U[3] * w + pr, Hs * w};
-            if constexpr (H == 1) {
-                // the reference-frame map J^-1 F is applied per variable in
-                // phase C (balanced across threads)
-#pragma unroll
-                for (int k = 0; k < 15; ++k) sl[k] = F[k];
-            } else {
-                // H > 1: J^-1 F here (phase C threads hold no J^-1)
-                T jj[9];
-#pragma unroll
-                for (int k = 0; k < 9; ++k) jj[k] = T(G[k * E + ee]);
-#pragma unroll
-                for (int d = 0; d < 3; ++d)
-#pragma unroll
-                    for (int var = 0; var < 5; ++var)
-                        sl[d * 5 + var] = jj[3 * d] * F[var] + jj[3 * d + 1] * F[5 + var] + jj[3 * d + 2] * F[10 + var];
-            }
+            for (int k = 0; k < 9; ++k) ji[k] = T(G[k * E + e]);
         }
-        __syncthreads();
-        // phase C (volume): contravariant flux of variable v against the
-        // weighted derivative table, this part's basis functions (MOMENTS:
-        // the physical flux of variable v against the weighted lower
-        // monomials; J^-1 and the derivative identity after the last chunk)
-        if constexpr (MOMENTS) {
+        sfor<NCH>([&](auto ch) {
+            constexpr int q0 = ch * QC;
+            constexpr int nq = (NQV - q0) < QC ? (NQV - q0) : QC;
+            // phase A: traces of variable v (H > 1: partial sums of this part,
+            // added in phase B in part order)
             if (live) {
-                sfor<nq>([&](auto qq) {
-                    const T* sl = X + (qq * E + e) * XS;
-                    const T fx = sl[v], fy = sl[5 + v], fz = sl[10 + v];
-                    sfor<NBL>([&](auto j) {
-                        const T wm = TAB(WV, T, (q0 + qq) * NB + j);
-                        mom[j][0] += wm * fx;
-                        mom[j][1] += wm * fy;
-                        mom[j][2] += wm * fz;
+                hsel(h, [&](auto hc) {
+                    sfor<nq>([&](auto qq) {
+                        T u = T(0);
+                        sfor<NH>([&](auto i) { u += TAB(VB, T, (q0 + qq) * NB + hc * NH + i) * T(c[i]); });
+                        X[(qq * E + e) * XS + hc * 5 + v] = u;
                     });
                 });
             }
-        } else if (live) {
-            hsel(h, [&](auto hc) {
-                sfor<nq>([&](auto qq) {
-                    const T* sl = X + (qq * E + e) * XS;
-                    T fd[3];
-                    if constexpr (H == 1) {
+            __syncthreads();
+            // phase B: thread (e, q): Euler flux (and J^-1 F when H > 1)
+            for (int p = t; p < nq * E; p += ETHREADS) {
+                const int qq = p / E;
+                const int ee = p - qq * E;
+                if (ee >= ne) continue;
+                T* sl = X + (qq * E + ee) * XS;
+                T U[5];
+#pragma unroll
+                for (int k = 0; k < 5; ++k) U[k] = sl[k];
+                if constexpr (H > 1) {
+#pragma unroll
+                    for (int hh = 1; hh < H; ++hh)
+#pragma unroll
+                        for (int k = 0; k < 5; ++k) U[k] += sl[hh * 5 + k];
+                }
+                T u, vv, w;
+                const T pr = (U[0] > T(0)) ? prim(U, gam, u, vv, w) : T(-1);
+                if (!(pr > T(0))) {
+                    flag(err, 1, uint32_t(e0 + ee));
+#pragma unroll
+                    for (int k = 0; k < XS; ++k) sl[k] = T(0);
+                    continue;
+                }
+                // physical flux F[d][var]
+                const T Hs = U[4] + pr;
+                T F[15] = {U[1], U[1] * u + pr, U[1] * vv, U[1] * w, Hs * u,
+                           U[2], U[2] * u, U[2] * vv + pr, U[2] * w, Hs * vv,
+                           U[3], U[3] * u, U[3] * vv, U[3] * w + pr, Hs * w};
+                if constexpr (H == 1) {
+                    // the reference-frame map J^-1 is applied per variable later
+#pragma unroll
+                    for (int k = 0; k < 15; ++k) sl[k] = F[k];
+                } else {
+                    // H > 1: J^-1 F here (phase C threads hold no J^-1)
+                    T jj[9];
+#pragma unroll
+                    for (int k = 0; k < 9; ++k) jj[k] = T(G[k * E + ee]);
+#pragma unroll
+                    for (int d = 0; d < 3; ++d)
+#pragma unroll
+                        for (int var = 0; var < 5; ++var)
+                            sl[d * 5 + var] =
+                                jj[3 * d] * F[var] + jj[3 * d + 1] * F[5 + var] + jj[3 * d + 2] * F[10 + var];
+                }
+            }
+            __syncthreads();
+            // phase C (volume): contravariant flux of variable v against the
+            // weighted derivative table, this part's basis functions (MOMENTS:
+            // the physical flux of variable v against the weighted lower
+            // monomials; J^-1 and the derivative identity after the last chunk)
+            if constexpr (MOMENTS) {
+                if (live) {
+                    sfor<nq>([&](auto qq) {
+                        const T* sl = X + (qq * E + e) * XS;
                         const T fx = sl[v], fy = sl[5 + v], fz = sl[10 + v];
-                        fd[0] = ji[0] * fx + ji[1] * fy + ji[2] * fz;
-                        fd[1] = ji[3] * fx + ji[4] * fy + ji[5] * fz;
-                        fd[2] = ji[6] * fx + ji[7] * fy + ji[8] * fz;
-                    } else {
-                        fd[0] = sl[v];
-                        fd[1] = sl[5 + v];
-                        fd[2] = sl[10 + v];
-                    }
-                    sfor<NH>([&](auto i) {
-                        constexpr int ig = hc * NH + i;
-                        sfor<3>([&](auto d) {
-                            if constexpr (expt(ig, d) > 0)
-                                acc[i] += TAB(VD, T, ((q0 + qq) * NB + ig) * 3 + d) * fd[d];
+                        sfor<NBL>([&](auto j) {
+                            const T wm = TAB(WV, T, (q0 + qq) * NB + j);
+                            mom[j][0] += wm * fx;
+                            mom[j][1] += wm * fy;
+                            mom[j][2] += wm * fz;
+                        });
+                    });
+                }
+            } else if (live) {
+                hsel(h, [&](auto hc) {
+                    sfor<nq>([&](auto qq) {
+                        const T* sl = X + (qq * E + e) * XS;
+                        T fd[3];
+                        if constexpr (H == 1) {
+                            const T fx = sl[v], fy = sl[5 + v], fz = sl[10 + v];
+                            fd[0] = ji[0] * fx + ji[1] * fy + ji[2] * fz;
+                            fd[1] = ji[3] * fx + ji[4] * fy + ji[5] * fz;
+                            fd[2] = ji[6] * fx + ji[7] * fy + ji[8] * fz;
+                        } else {
+                            fd[0] = sl[v];
+                            fd[1] = sl[5 + v];
+                            fd[2] = sl[10 + v];
+                        }
+                        sfor<NH>([&](auto i) {
+                            constexpr int ig = hc * NH + i;
+                            sfor<3>([&](auto d) {
+                                if constexpr (expt(ig, d) > 0)
+                                    acc[i] += TAB(VD, T, ((q0 + qq) * NB + ig) * 3 + d) * fd[d];
+                            });
                         });
                     });
                 });
-            });
-        }
-        __syncthreads();
-    });
-    if constexpr (MOMENTS) {
-        // sum_q VD[q][i][d] (J^-1 F)_d = sum_d alpha_{i,d} sum_k Jinv[d][k] MOM[i - e_d][k]
-        T mj[NBL][3];
-#pragma unroll
-        for (int j = 0; j < NBL; ++j)
-#pragma unroll
-            for (int d = 0; d < 3; ++d)
-                mj[j][d] = ji[3 * d] * mom[j][0] + ji[3 * d + 1] * mom[j][1] + ji[3 * d + 2] * mom[j][2];
-        sfor<NB>([&](auto i) {
-            T sum = T(0);
-            sfor<3>([&](auto d) {
-                constexpr int al = expt(i, d);
-                if constexpr (al > 0) {
-                    constexpr int lo = mono_index(expt(i, 0) - (d == 0), expt(i, 1) - (d == 1), expt(i, 2) - (d == 2));
-                    sum += T(al) * mj[lo][d];
-                }
-            });
-            acc[i] = sum;
-        });
-    }
-
-    // P3: the u0 tile is not held in registers through the volume phases;
-    // one TMA copy into the freed state / X region, in flight during the
-    // gather and the solve (each thread later reads, then overwrites with
-    // its output, only its own entries)
-    if constexpr (U0_TMA) {
-        if (need_u0 && t == 0 && ne > 0) {
-            const uint32_t bs = uint32_t(ne) * RS * 8;
-            fence_proxy_async();
-            mbar_arrive_expect_tx(bar, bs);
-            bulk_g2s(S, a.u0 + e0 * RS, bs, bar);
-        }
-    }
-    // face gather, mass solve, RK update
-    mbar_wait(bar + 1, 0);
-    double accd[NH];
-    if (live) {
-#pragma unroll
-        for (int i = 0; i < NH; ++i) accd[i] = double(acc[i]);
-        hsel(h, [&](auto hc) {
-            sfor<4>([&](auto s) {
-                const T* hrec =
-                    ES ? HT + size_t(e) * EREC + s * HSE + v * NQF : HT + size_t(s * E + e) * HSS + v * NQF;
-                T hq[NQF];
-                if constexpr (ES) {
-#pragma unroll
-                    for (int q = 0; q < NQF; ++q) hq[q] = hrec[q];
-                } else if constexpr (sizeof(T) == 8) {
-                    // record rows are 16-byte aligned: 128-bit loads on aligned pairs
-                    if ((v * NQF) & 1) ld_rec<NQF, 1>(hrec, hq);
-                    else ld_rec<NQF, 0>(hrec, hq);
-                } else {
-#pragma unroll
-                    for (int q = 0; q < NQF; ++q) hq[q] = hrec[q];
-                }
-                T fa[NH];
-                face_moments<T, s, hc * NH, NH>(hq, fa);
-                const double fc = G[(9 + s) * E + e];
-#pragma unroll
-                for (int i = 0; i < NH; ++i) accd[i] -= fc * double(fa[i]);
-            });
-        });
-    }
-    double full[H == 1 ? 1 : NB];
-    if constexpr (H > 1) {
-        // assemble the (v, e) residual vector of all parts (records consumed)
-        __syncthreads();
-        if (live) {
-#pragma unroll
-            for (int i = 0; i < NH; ++i) Z[(v * E + e) * NB + jb + i] = accd[i];
-        }
-        __syncthreads();
-        if (live) {
-#pragma unroll
-            for (int k = 0; k < NB; ++k) full[k] = Z[(v * E + e) * NB + k];
-        }
-    }
-    if (live) {
-        double r[NH];
-        hsel(h, [&](auto hc) {
-            sfor<NH>([&](auto j) {
-                double z = 0.0;
-                if constexpr (H == 1) {
-                    sfor<NB>([&](auto k) { z += MINV_T[j * NB + k] * accd[k]; });
-                } else {
-                    sfor<NB>([&](auto k) { z += MINV_T[(hc * NH + j) * NB + k] * full[k]; });
-                }
-                r[j] = z;
-            });
-        });
-        if (a.res) {
-#pragma unroll
-            for (int j = 0; j < NH; ++j) a.res[gid * RS + v * NB + jb + j] = r[j];
-        }
-        if (a.norm_partial && h == 0) RED[v * E + e] = G[14 * E + e] * r[0] * r[0];
-        if (a.combine >= 0) {
-            if constexpr (U0_TMA) {
-                if (need_u0) mbar_wait(bar, 1);
             }
-            const double dt = a.dt_is_vector ? a.dt[gid] : a.dt[0];
-            double mean = 0.0;
-            double outr[NH];
+            __syncthreads();
+        });
+        if constexpr (MOMENTS) {
+            // sum_q VD[q][i][d] (J^-1 F)_d = sum_d alpha_{i,d} sum_k Jinv[d][k] MOM[i - e_d][k]
+            T mj[NBL][3];
+#pragma unroll
+            for (int j = 0; j < NBL; ++j)
+#pragma unroll
+                for (int d = 0; d < 3; ++d)
+                    mj[j][d] = ji[3 * d] * mom[j][0] + ji[3 * d + 1] * mom[j][1] + ji[3 * d + 2] * mom[j][2];
+            sfor<NB>([&](auto i) {
+                T sum = T(0);
+                sfor<3>([&](auto d) {
+                    constexpr int al = expt(i, d);
+                    if constexpr (al > 0) {
+                        constexpr int lo =
+                            mono_index(expt(i, 0) - (d == 0), expt(i, 1) - (d == 1), expt(i, 2) - (d == 2));
+                        sum += T(al) * mj[lo][d];
+                    }
+                });
+                acc[i] = sum;
+            });
+        }
+
+        // the u0 tile is not held in registers through the volume phases:
+        // one TMA copy into the freed X region, in flight during the gather
+        // and the solve (each thread later reads, then overwrites with its
+        // output, only its own entries)
+        if constexpr (U0_TMA) {
+            if (need_u0 && t == 0 && ne > 0) {
+                const uint32_t bs = uint32_t(ne) * RS * 8;
+                fence_proxy_async();
+                mbar_arrive_expect_tx(bar + 3, bs);
+                bulk_g2s(S, a.u0 + e0 * RS, bs, bar + 3);
+            }
+        }
+        // face gather, mass solve, RK update
+        mbar_wait(bar + 2, it & 1);
+        double accd[NH];
+        if (live) {
+#pragma unroll
+            for (int i = 0; i < NH; ++i) accd[i] = double(acc[i]);
             hsel(h, [&](auto hc) {
-                sfor<NH>([&](auto j) {
-                    double u0j = 0.0;
-                    if (need_u0) {
-                        if constexpr (!U0_TMA) u0j = u0r[j];
-                        else u0j = S[e * RS + v * NB + hc * NH + j];  // u0 tile (TMA, above)
-                    }
-                    double o;
-                    if (a.combine == 1) {
-                        o = 0.5 * ((u0j + c[j]) + dt * r[j]);
+                sfor<4>([&](auto s) {
+                    const T* hrec =
+                        ES ? HT + size_t(e) * EREC + s * HSE + v * NQF : HT + size_t(s * E + e) * HSS + v * NQF;
+                    T hq[NQF];
+                    if constexpr (ES) {
+#pragma unroll
+                        for (int q = 0; q < NQF; ++q) hq[q] = hrec[q];
+                    } else if constexpr (sizeof(T) == 8) {
+                        // record rows are 16-byte aligned: 128-bit loads on aligned pairs
+                        if ((v * NQF) & 1) ld_rec<NQF, 1>(hrec, hq);
+                        else ld_rec<NQF, 0>(hrec, hq);
                     } else {
-                        o = a.b * (c[j] + dt * r[j]);
-                        if (a.a != 0.0) o = a.a * u0j + o;
+#pragma unroll
+                        for (int q = 0; q < NQF; ++q) hq[q] = hrec[q];
                     }
-                    outr[j] = o;
-                    mean += MEAN_T[hc * NH + j] * o;
+                    T fa[NH];
+                    face_moments<T, s, hc * NH, NH>(hq, fa);
+                    const double fc = G[(9 + s) * E + e];
+#pragma unroll
+                    for (int i = 0; i < NH; ++i) accd[i] -= fc * double(fa[i]);
                 });
             });
-            if constexpr (H == 1 && (NB % 2) == 0) {
-#pragma unroll
-                for (int j = 0; j < NB; j += 2)
-                    *reinterpret_cast<double2*>(S + e * RS + v * NB + j) = make_double2(outr[j], outr[j + 1]);
-            } else {
-#pragma unroll
-                for (int j = 0; j < NH; ++j) S[e * RS + v * NB + jb + j] = outr[j];
-            }
-            RED[5 * E + h * 5 * E + v * E + e] = mean;
         }
-    }
-    fence_proxy_async();
-    __syncthreads();
-    if (t == 0 && a.combine >= 0 && ne > 0) bulk_s2g(a.out + e0 * RS, S, uint32_t(ne) * RS * 8);
-    // epilogues without a trailing barrier: fixed-order shuffle trees over
-    // the (variable, element) pairs held by threads t < 5E (vn = t / E)
-    const int lane = t & 31;
-    const int vn = t / E;
-    if (a.norm_partial && t < 5 * E) {
-        // partial sum over the tile of vol * res_0^2 per variable; warp w
-        // holds variable (32 w) / E (E >= 32) or two variables (E == 16)
-        constexpr int W = E < 32 ? E : 32;
-        double x = (e < ne) ? RED[vn * E + e] : 0.0;
+        double full[H == 1 ? 1 : NB];
+        if constexpr (H > 1) {
+            // assemble the (v, e) residual vector of all parts (records consumed)
+            __syncthreads();
+            if (live) {
 #pragma unroll
-        for (int o = W / 2; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-        if (E <= 32) {
-            if ((lane % W) == 0) a.norm_partial[int64_t(blockIdx.x) * 5 + vn] = x;
-        } else {  // E == 64: two warps per variable, combined in a fixed order
-            __shared__ double half2[10];
-            if (lane == 0) half2[(t / 32)] = x;
-            __syncwarp();
-            asm volatile("bar.sync 1, %0;" ::"r"(5 * E));  // the 5E threads of this epilogue
-            if (t < 5) a.norm_partial[int64_t(blockIdx.x) * 5 + t] = half2[2 * t] + half2[2 * t + 1];
-        }
-    }
-    if (a.combine >= 0 && (a.dt_next || a.dt_vec_out) && t < E) {
-        // CFL dt of the new cell mean (hodg/timestepping.py:121-134), 3D;
-        // threads t < E (element t), no other warp waits
-        double dt = 0.0;
-        bool okdt = false;
-        if (e < ne) {
-            double mm[5];
-#pragma unroll
-            for (int k = 0; k < 5; ++k) {
-                mm[k] = RED[5 * E + k * E + e];
-#pragma unroll
-                for (int hh = 1; hh < H; ++hh) mm[k] += RED[5 * E + hh * 5 * E + k * E + e];
+                for (int i = 0; i < NH; ++i) Z[(v * E + e) * NB + jb + i] = accd[i];
             }
-            const double m0 = mm[0], m1 = mm[1], m2 = mm[2], m3 = mm[3], m4 = mm[4];
-            if (!(m0 > 0.0)) {
-                flag(err, 2, uint32_t(gid));
-            } else {
-                const double ri = 1.0 / m0;
-                const double u = m1 * ri, vv = m2 * ri, w = m3 * ri;
-                const double p = (m.gamma - 1.0) * (m4 - 0.5 * m0 * (u * u + vv * vv + w * w));
-                if (!(p > 0.0)) {
+            __syncthreads();
+            if (live) {
+#pragma unroll
+                for (int k = 0; k < NB; ++k) full[k] = Z[(v * E + e) * NB + k];
+            }
+        }
+        if constexpr (EPERSIST) {
+            // the records are consumed: the next tile's inputs stream into the
+            // region during this tile's solve and epilogue
+            __syncthreads();
+            if (t == 0 && tile + gridDim.x < ntiles) {
+                fence_proxy_async();
+                issue_inputs(tile + gridDim.x, gbuf ^ 1);
+            }
+        }
+        if (live) {
+            double r[NH];
+            hsel(h, [&](auto hc) {
+                sfor<NH>([&](auto j) {
+                    double z = 0.0;
+                    if constexpr (H == 1) {
+                        sfor<NB>([&](auto k) { z += MINV_T[j * NB + k] * accd[k]; });
+                    } else {
+                        sfor<NB>([&](auto k) { z += MINV_T[(hc * NH + j) * NB + k] * full[k]; });
+                    }
+                    r[j] = z;
+                });
+            });
+            if (a.res) {
+#pragma unroll
+                for (int j = 0; j < NH; ++j) a.res[gid * RS + v * NB + jb + j] = r[j];
+            }
+            if (a.norm_partial && h == 0) RED[v * E + e] = G[14 * E + e] * r[0] * r[0];
+            if (a.combine >= 0) {
+                if constexpr (U0_TMA) {
+                    if (need_u0) mbar_wait(bar + 3, it & 1);
+                }
+                const double dt = a.dt_is_vector ? a.dt[gid] : a.dt[0];
+                double mean = 0.0;
+                double outr[NH];
+                hsel(h, [&](auto hc) {
+                    sfor<NH>([&](auto j) {
+                        double u0j = 0.0;
+                        if (need_u0) {
+                            if constexpr (!U0_TMA) u0j = u0r[j];
+                            else u0j = S[e * RS + v * NB + hc * NH + j];  // u0 tile (TMA, above)
+                        }
+                        double o;
+                        if (a.combine == 1) {
+                            o = 0.5 * ((u0j + c[j]) + dt * r[j]);
+                        } else {
+                            o = a.b * (c[j] + dt * r[j]);
+                            if (a.a != 0.0) o = a.a * u0j + o;
+                        }
+                        outr[j] = o;
+                        mean += MEAN_T[hc * NH + j] * o;
+                    });
+                });
+                if constexpr (H == 1 && (NB % 2) == 0) {
+#pragma unroll
+                    for (int j = 0; j < NB; j += 2)
+                        *reinterpret_cast<double2*>(S + e * RS + v * NB + j) = make_double2(outr[j], outr[j + 1]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < NH; ++j) S[e * RS + v * NB + jb + j] = outr[j];
+                }
+                if constexpr (sizeof(T) == 4) {
+                    if (shadow) {
+#pragma unroll
+                        for (int j = 0; j < NH; ++j) S32[e * RSF + v * NB + jb + j] = float(outr[j]);
+                    }
+                }
+                RED[5 * E + h * 5 * E + v * E + e] = mean;
+            }
+        }
+        fence_proxy_async();
+        __syncthreads();
+        if (t == 0 && a.combine >= 0 && ne > 0) {
+            bulk_s2g(a.out + e0 * RS, S, uint32_t(ne) * RS * 8);
+            if (shadow) bulk_s2g(a.out32 + e0 * RSF, S32, uint32_t(ne) * RSF * 4);
+        }
+        // epilogues without a trailing barrier: fixed-order shuffle trees over
+        // the (variable, element) pairs held by threads t < 5E (vn = t / E)
+        const int lane = t & 31;
+        const int vn = t / E;
+        if (a.norm_partial && t < 5 * E) {
+            // partial sum over the tile of vol * res_0^2 per variable; warp w
+            // holds variable (32 w) / E (E >= 32) or two variables (E == 16)
+            constexpr int W = E < 32 ? E : 32;
+            double x = (e < ne) ? RED[vn * E + e] : 0.0;
+#pragma unroll
+            for (int o = W / 2; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+            if (E <= 32) {
+                if ((lane % W) == 0) a.norm_partial[tile * 5 + vn] = x;
+            } else {  // E == 64: two warps per variable, combined in a fixed order
+                __shared__ double half2[10];
+                if (lane == 0) half2[(t / 32)] = x;
+                __syncwarp();
+                asm volatile("bar.sync 1, %0;" ::"r"(5 * E));  // the 5E threads of this epilogue
+                if (t < 5) a.norm_partial[tile * 5 + t] = half2[2 * t] + half2[2 * t + 1];
+                asm volatile("bar.sync 1, %0;" ::"r"(5 * E));  // half2 read before the next tile
+            }
+        }
+        if (a.combine >= 0 && (a.dt_next || a.dt_vec_out) && t < E) {
+            // CFL dt of the new cell mean (hodg/timestepping.py:121-134), 3D;
+            // threads t < E (element t), no other warp waits
+            double dt = 0.0;
+            bool okdt = false;
+            if (e < ne) {
+                double mm[5];
+#pragma unroll
+                for (int k = 0; k < 5; ++k) {
+                    mm[k] = RED[5 * E + k * E + e];
+#pragma unroll
+                    for (int hh = 1; hh < H; ++hh) mm[k] += RED[5 * E + hh * 5 * E + k * E + e];
+                }
+                const double m0 = mm[0], m1 = mm[1], m2 = mm[2], m3 = mm[3], m4 = mm[4];
+                if (!(m0 > 0.0)) {
                     flag(err, 2, uint32_t(gid));
                 } else {
-                    const double speed = sqrt(u * u + vv * vv + w * w) + sqrt(m.gamma * p * ri);
-                    dt = a.cfl * G[13 * E + e] / ((2.0 * ORDER + 1.0) * speed);
-                    okdt = true;
+                    const double ri = 1.0 / m0;
+                    const double u = m1 * ri, vv = m2 * ri, w = m3 * ri;
+                    const double p = (m.gamma - 1.0) * (m4 - 0.5 * m0 * (u * u + vv * vv + w * w));
+                    if (!(p > 0.0)) {
+                        flag(err, 2, uint32_t(gid));
+                    } else {
+                        const double speed = sqrt(u * u + vv * vv + w * w) + sqrt(m.gamma * p * ri);
+                        dt = a.cfl * G[13 * E + e] / ((2.0 * ORDER + 1.0) * speed);
+                        okdt = true;
+                    }
                 }
+                if (a.dt_vec_out) a.dt_vec_out[gid] = dt;
             }
-            if (a.dt_vec_out) a.dt_vec_out[gid] = dt;
-        }
-        if (a.dt_next) {
-            unsigned long long bits = okdt ? static_cast<unsigned long long>(__double_as_longlong(dt))
-                                           : 0x7FF0000000000000ull;
-            constexpr int W = E < 32 ? E : 32;
-            constexpr unsigned mask = E < 32 ? ((1u << E) - 1u) : 0xffffffffu;  // lanes t < E
+            if (a.dt_next) {
+                unsigned long long bits = okdt ? static_cast<unsigned long long>(__double_as_longlong(dt))
+                                               : 0x7FF0000000000000ull;
+                constexpr int W = E < 32 ? E : 32;
+                constexpr unsigned mask = E < 32 ? ((1u << E) - 1u) : 0xffffffffu;  // lanes t < E
 #pragma unroll
-            for (int o = W / 2; o > 0; o >>= 1) {
-                const unsigned long long other = __shfl_xor_sync(mask, bits, o);
-                bits = other < bits ? other : bits;
+                for (int o = W / 2; o > 0; o >>= 1) {
+                    const unsigned long long other = __shfl_xor_sync(mask, bits, o);
+                    bits = other < bits ? other : bits;
+                }
+                if ((lane % W) == 0) atomicMin(a.dt_next, bits);
             }
-            if ((lane % W) == 0) atomicMin(a.dt_next, bits);
         }
+        // the output tile is read by the bulk store before the next tile's
+        // volume phase overwrites the region
+        if (t == 0 && a.combine >= 0 && ne > 0) bulk_wait_read();
+        if constexpr (!EPERSIST) break;  // one tile per CTA
     }
-    if (t == 0 && a.combine >= 0 && ne > 0) bulk_wait_read();
 }
 
 // ---------------------------------------------------------------------------
@@ -1089,29 +1188,38 @@ static int launch_maybe_pdl(const hodg_mesh_desc& m, K kernel, int64_t nblk, int
     return cudaGetLastError() == cudaSuccess ? HODG_OK : HODG_ECUDA;
 }
 
-template <typename T, bool BND, bool ES>
-static int launch_face_k(const hodg_mesh_desc& m, const double* state, void* hbuf, uint32_t* err, cudaStream_t st,
+template <typename T, bool BND, bool ES, typename R>
+static int launch_face_k(const hodg_mesh_desc& m, const R* state, void* hbuf, uint32_t* err, cudaStream_t st,
                          int64_t fb, int64_t fe) {
-    const size_t sm = face_smem_bytes<T>();
+    const size_t sm = face_smem_bytes<T, R>();
     static LaunchCache lc;
     int cap = 0;
-    if (launch_setup(lc, face_flux_kernel<T, BND, ES>, FACE_THREADS, sm, &cap) != HODG_OK) return HODG_ECUDA;
+    if (launch_setup(lc, face_flux_kernel<T, BND, ES, R>, FACE_THREADS, sm, &cap) != HODG_OK) return HODG_ECUDA;
     const int64_t ntiles = (fe - fb + FT - 1) / FT;
     const int64_t nblk = ntiles < cap ? ntiles : cap;  // persistent CTAs loop over tiles
-    return launch_maybe_pdl(m, face_flux_kernel<T, BND, ES>, nblk, FACE_THREADS, sm, st, m, state,
+    return launch_maybe_pdl(m, face_flux_kernel<T, BND, ES, R>, nblk, FACE_THREADS, sm, st, m, state,
                             static_cast<T*>(hbuf), err, fb, fe);
 }
 
 // interior_only: every face in [fb, fe) has a right element (no boundary
 // state code in the kernel)
-template <typename T>
-static int launch_face(const hodg_mesh_desc& m, const double* state, void* hbuf, uint32_t* err, cudaStream_t st,
+template <typename T, typename R>
+static int launch_face(const hodg_mesh_desc& m, const R* state, void* hbuf, uint32_t* err, cudaStream_t st,
                        int64_t fb, int64_t fe, int interior_only, int es) {
     if (es)
-        return interior_only ? launch_face_k<T, false, true>(m, state, hbuf, err, st, fb, fe)
-                             : launch_face_k<T, true, true>(m, state, hbuf, err, st, fb, fe);
-    return interior_only ? launch_face_k<T, false, false>(m, state, hbuf, err, st, fb, fe)
-                         : launch_face_k<T, true, false>(m, state, hbuf, err, st, fb, fe);
+        return interior_only ? launch_face_k<T, false, true, R>(m, state, hbuf, err, st, fb, fe)
+                             : launch_face_k<T, true, true, R>(m, state, hbuf, err, st, fb, fe);
+    return interior_only ? launch_face_k<T, false, false, R>(m, state, hbuf, err, st, fb, fe)
+                         : launch_face_k<T, true, false, R>(m, state, hbuf, err, st, fb, fe);
+}
+
+// FP64 state -> its FP32 shadow (rows [0, n_rows), padding zeroed)
+__global__ void state_to_f32_kernel(const double* __restrict__ in, int64_t n_rows, float* __restrict__ out) {
+    const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= n_rows * RSF) return;
+    const int64_t r = k / RSF;
+    const int j = int(k - r * RSF);
+    out[k] = j < 5 * NB ? float(in[r * RS + j]) : 0.0f;
 }
 
 template <typename T, bool ES>
@@ -1132,7 +1240,8 @@ static int launch_elem_k(const hodg_mesh_desc& m, const void* hbuf, const hodg_s
         static LaunchCache lc;
         int cap = 0;
         if (launch_setup(lc, elem_stage_kernel<T, ES>, ETHREADS, sm, &cap) != HODG_OK) return HODG_ECUDA;
-        const int64_t nblk = (m.n_elems + E - 1) / E;
+        const int64_t ntiles = (m.n_elems + E - 1) / E;
+        const int64_t nblk = EPERSIST && ntiles > cap ? cap : ntiles;  // persistent CTAs loop over tiles
         return launch_maybe_pdl(m, elem_stage_kernel<T, ES>, nblk, ETHREADS, sm, st, m, static_cast<const T*>(hbuf),
                                 a, err);
     }
@@ -1152,9 +1261,24 @@ int HODG_CAT(hodg_launch_face_p, ORDER)(const hodg_mesh_desc& m, int prec, const
                                          uint32_t* err, cudaStream_t st, int64_t fb, int64_t fe, int interior,
                                          int es) {
     using namespace hodg::HODG_CAT(ord, ORDER);
-    return prec == HODG_PREC_MIXED ? launch_face<float>(m, state, hbuf, err, st, fb, fe, interior, es)
-                                   : launch_face<double>(m, state, hbuf, err, st, fb, fe, interior, es);
+    return prec == HODG_PREC_MIXED ? launch_face<float, double>(m, state, hbuf, err, st, fb, fe, interior, es)
+                                   : launch_face<double, double>(m, state, hbuf, err, st, fb, fe, interior, es);
 }
+
+int HODG_CAT(hodg_launch_face32_p, ORDER)(const hodg_mesh_desc& m, const float* state32, void* hbuf, uint32_t* err,
+                                           cudaStream_t st, int64_t fb, int64_t fe, int interior, int es) {
+    using namespace hodg::HODG_CAT(ord, ORDER);
+    return launch_face<float, float>(m, state32, hbuf, err, st, fb, fe, interior, es);
+}
+
+int HODG_CAT(hodg_launch_to_f32_p, ORDER)(const double* rows, int64_t n_rows, float* rows32, cudaStream_t st) {
+    using namespace hodg::HODG_CAT(ord, ORDER);
+    const int64_t n = n_rows * RSF;
+    if (n > 0) state_to_f32_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(rows, n_rows, rows32);
+    return cudaGetLastError() == cudaSuccess ? HODG_OK : HODG_ECUDA;
+}
+
+int HODG_CAT(hodg_state32_stride_p, ORDER)() { return hodg::HODG_CAT(ord, ORDER)::RSF; }
 
 int HODG_CAT(hodg_launch_elem_p, ORDER)(const hodg_mesh_desc& m, int prec, const void* hbuf,
                                          const hodg_stage_args& a, uint32_t* err, cudaStream_t st, int es) {

@@ -255,7 +255,30 @@ class Discretization:
                           _lib.ptr(self.err), _lib.stream_ptr(stream)), "hodg_face_flux_range")
         return hbuf
 
-    def face_flux_split(self, rows, prec, hbuf, side):
+    # -- mixed precision: the FP32 shadow of the state ----------------------
+    @property
+    def rs32(self) -> int:
+        return int(self.L.hodg_state32_row_stride(self.order))
+
+    def new_state32(self, rows=None):
+        return _torch().zeros((self.n_rows if rows is None else rows, self.rs32), dtype=_torch().float32,
+                              device=self.device)
+
+    def shadow_of(self, rows, out32):
+        """FP32 shadow of FP64 state rows (all rows, ghosts included)."""
+        _lib.check(self.L.hodg_state_to_f32(self.handle, _lib.ptr(rows), rows.shape[0], _lib.ptr(out32),
+                                            _lib.stream_ptr()), "hodg_state_to_f32")
+        return out32
+
+    def face_flux32(self, rows32, hbuf, stream=None, f_begin=0, f_end=None):
+        """Mixed-precision face kernel reading the FP32 shadow rows."""
+        for lo, hi, interior in self.face_segments(f_begin, f_end):
+            fn = self.L.hodg_face_flux_range32_es if hbuf.dim() == 1 else self.L.hodg_face_flux_range32
+            _lib.check(fn(self.handle, _lib.ptr(rows32), _lib.ptr(hbuf), int(lo), int(hi), interior,
+                          _lib.ptr(self.err), _lib.stream_ptr(stream)), "hodg_face_flux_range32")
+        return hbuf
+
+    def face_flux_split(self, rows, prec, hbuf, side, rows32=None):
         """face_flux over all faces with the boundary (+ partition) range on
         the `side` stream, issued after the interior range: its CTAs take the
         SM slots the persistent interior kernel frees in its tail instead of
@@ -263,12 +286,20 @@ class Discretization:
         into the current stream."""
         torch = _torch()
         segs = self.face_segments()
+
+        def run(stream=None, f_begin=0, f_end=None):
+            if rows32 is not None:
+                self.face_flux32(rows32, hbuf, stream=stream, f_begin=f_begin, f_end=f_end)
+            else:
+                self.face_flux(rows, prec, hbuf, stream=stream, f_begin=f_begin, f_end=f_end)
+
         if side is None or len(segs) < 2:
-            return self.face_flux(rows, prec, hbuf)
+            run()
+            return hbuf
         cur = torch.cuda.current_stream()
         side.wait_stream(cur)
-        self.face_flux(rows, prec, hbuf, f_begin=segs[0][0], f_end=segs[0][1])
-        self.face_flux(rows, prec, hbuf, stream=side, f_begin=segs[1][0], f_end=self.nf)
+        run(f_begin=segs[0][0], f_end=segs[0][1])
+        run(stream=side, f_begin=segs[1][0], f_end=self.nf)
         cur.wait_stream(side)
         return hbuf
 

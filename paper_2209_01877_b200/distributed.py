@@ -50,7 +50,7 @@ class DistributedStepper(Stepper):
         # (no host sync per step), so the host runs ahead of the GPU; NCCL
         # point-to-point inside CUDA-graph capture is not used (a captured
         # self-exchange hung on the B200 test box)
-        super().__init__(disc, scheme, prec, "global", cfl, log_norms=log_norms, use_graph=False)
+        super().__init__(disc, scheme, prec, "global", cfl, log_norms=log_norms, use_graph=False, shadow=False)
         self.part = part
         self.group = group
         self.native = halo == "native"

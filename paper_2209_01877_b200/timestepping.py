@@ -190,7 +190,7 @@ class Stepper:
     """
 
     def __init__(self, disc: Discretization, scheme="rk3", prec=_lib.PREC_F64, dt_mode="global", cfl=0.3,
-                 log_norms=True, use_graph=True, layout="auto"):
+                 log_norms=True, use_graph=True, layout="auto", shadow=None):
         torch = _torch()
         if layout not in ("auto", "elem", "face"):
             raise ValueError(f"unknown record layout {layout!r}")
@@ -217,6 +217,14 @@ class Stepper:
         # boundary faces concurrent with the interior tail (HODG_OVERLAP_BND=0: serial)
         self._side = torch.cuda.Stream(device=dev) if os.environ.get("HODG_OVERLAP_BND", "1") != "0" else None
         self.capture_mode = "global"
+        # mixed precision: the element kernel also writes an FP32 shadow of
+        # each stage's state, which the face kernel reads (no per-row FP64 ->
+        # FP32 conversion, half the row bytes); off with shadow=False or
+        # HODG_SHADOW=0, and for partitioned runs (FP64 ghost rows)
+        if shadow is None:
+            shadow = os.environ.get("HODG_SHADOW", "1") != "0"
+        self.shadow = bool(shadow)
+        self.A32 = self.B32 = None
 
     # -- state in / out ----------------------------------------------------
     def load(self, state: DofState):
@@ -224,6 +232,19 @@ class Stepper:
         self.steps = 0
         self.parity = 0
         self.init_dt()
+        self._sync_shadow()
+
+    def _uses_shadow(self) -> bool:
+        return self.shadow and self.prec == _lib.PREC_MIXED
+
+    def _sync_shadow(self):
+        """(Re)build the FP32 shadow of A when the mixed kernels run."""
+        if not self._uses_shadow():
+            return
+        if self.A32 is None:
+            self.A32 = self.disc.new_state32()
+            self.B32 = self.disc.new_state32()
+        self.disc.shadow_of(self.A, self.A32)
 
     def state(self, iteration=0) -> DofState:
         return DofState(self.disc.from_reference(self.A), iteration)
@@ -299,6 +320,8 @@ class Stepper:
         if k == 0 and self.dt_mode == "global":
             s.dt_reset = C.c_void_p(self.slots.data_ptr() + 8 * (1 - parity))
         s.cfl = self.cfl
+        if self._uses_shadow():
+            s.out32 = _lib.ptr(self.A32 if last else self.B32)
         return s
 
     def _launch_step(self, parity):
@@ -306,7 +329,8 @@ class Stepper:
         n_st = len(SCHEMES[self.scheme])
         for k in range(n_st):
             us = self.A if k == 0 else self.B
-            d.face_flux_split(us, self.prec, self.hbuf, self._side)
+            us32 = (self.A32 if k == 0 else self.B32) if self._uses_shadow() else None
+            d.face_flux_split(us, self.prec, self.hbuf, self._side, rows32=us32)
             args = self._stage_args(k, parity)
             self._args.append(args)
             d.stage(self.prec, self.hbuf, args)
@@ -318,7 +342,10 @@ class Stepper:
         """Run the stage kernels once outside graph capture (first-launch
         attribute setup) without touching the state: residual into B."""
         d = self.disc
-        d.face_flux(self.A, self.prec, self.hbuf)
+        if self._uses_shadow():
+            d.face_flux32(self.A32, self.hbuf)
+        else:
+            d.face_flux(self.A, self.prec, self.hbuf)
         d.residual_rows(self.A, self.hbuf, self.prec, res=self.B)
 
     def launches_per_step(self) -> int:
@@ -520,6 +547,7 @@ def run(config: RunConfig, mesh: TetMesh | None = None) -> RunArtifacts:
             stepper.prec = want
             stepper.hbuf = stepper._records(want)
             stepper._graphs.clear()
+            stepper._sync_shadow()
         log = config.log_every and (it % config.log_every == 0 or it == config.max_iterations - 1)
         if config.dt_mode == "global":
             if host_dt:

@@ -371,3 +371,29 @@ def test_wing_against_oracle(P):
     u, hist, _ = S.run(spec)
     assert rel(art.final_state.coeffs.cpu().numpy(), u) <= FP64_TOL
     assert rel(np.array(art.history.res), np.array(hist.res)) <= FP64_TOL
+
+
+@pytest.mark.parametrize("order", [1, 2, 3])
+def test_mixed_fp32_shadow_bitwise(P, order):
+    """The mixed-precision stepper's FP32 state shadow (element kernel writes
+    it, face kernel reads it) rounds each coefficient once instead of at
+    every (face, side): the steps are bitwise those of the FP64-row path."""
+    import torch
+
+    from paper_2209_01877_b200 import _lib
+    from paper_2209_01877_b200.dg import _get_disc
+    from paper_2209_01877_b200.timestepping import Stepper
+
+    m = P.perturb_interior_nodes(P.generate_tet_box(4, bc=gpu_helpers.MIXED_BC), 0.1, 3)
+    gas, geo, bcs = gpu_setup(P, m, order)
+    _, c = oracle_state(m, order)
+    out = []
+    for shadow in (True, False):
+        st = Stepper(_get_disc(m, geo, gas, bcs), "rk3", _lib.PREC_MIXED, "global", 0.3, shadow=shadow)
+        st.load(P.DofState(torch.from_numpy(c).cuda()))
+        for _ in range(3):
+            st.step()
+        st.check(3)
+        out.append((st.A.clone(), st.norms.clone(), st.dt_value()))
+        assert (st.A32 is not None) == shadow
+    assert torch.equal(out[0][0], out[1][0]) and torch.equal(out[0][1], out[1][1]) and out[0][2] == out[1][2]
