@@ -213,17 +213,20 @@ int hodg_halo_exchange(hodg_halo* h, double* state, void* stream) {
         if (cudaGetLastError() != cudaSuccess) return HODG_ECUDA;
     }
     if (n.GroupStart() != ncclSuccess) return HODG_ECUDA;
-    for (size_t p = 0; p < h->peers.size(); ++p) {
-        if (h->recv_count[p] > 0 &&
-            n.Recv(state + h->recv_first[p] * h->rs, size_t(h->recv_count[p] * h->rs), ncclFloat64, h->peers[p],
-                   h->comm, st) != ncclSuccess)
-            return HODG_ECUDA;
-        if (h->send_count[p] > 0 &&
-            n.Send(h->sendbuf + h->send_off[p] * h->rs, size_t(h->send_count[p] * h->rs), ncclFloat64,
-                   h->peers[p], h->comm, st) != ncclSuccess)
-            return HODG_ECUDA;
+    // a failed Send / Recv still closes the group: an open group would batch
+    // every later NCCL call on this thread (the dt / norm all-reduces) into a
+    // group that never launches
+    bool ok = true;
+    for (size_t p = 0; p < h->peers.size() && ok; ++p) {
+        if (h->recv_count[p] > 0)
+            ok = n.Recv(state + h->recv_first[p] * h->rs, size_t(h->recv_count[p] * h->rs), ncclFloat64,
+                        h->peers[p], h->comm, st) == ncclSuccess;
+        if (ok && h->send_count[p] > 0)
+            ok = n.Send(h->sendbuf + h->send_off[p] * h->rs, size_t(h->send_count[p] * h->rs), ncclFloat64,
+                        h->peers[p], h->comm, st) == ncclSuccess;
     }
-    return n.GroupEnd() == ncclSuccess ? HODG_OK : HODG_ECUDA;
+    const bool closed = n.GroupEnd() == ncclSuccess;
+    return ok && closed ? HODG_OK : HODG_ECUDA;
 }
 
 int hodg_halo_allreduce(hodg_halo* h, void* buf, int64_t count, int kind, void* stream) {

@@ -73,7 +73,7 @@ constexpr int H = (ORDER == 3) ? HODG_H3 : (ORDER == 2 ? HODG_H2 : 1);
 // P1 and P2 run the warp-group element kernel (hodg_elem_warp.cuh): G = 6
 // elements per warp, lane (e, v); its element tile is the warp's group
 #ifndef HODG_WARP_ELEM_P1
-#define HODG_WARP_ELEM_P1 1
+#define HODG_WARP_ELEM_P1 0
 #endif
 #ifndef HODG_WARP_ELEM_P2
 #define HODG_WARP_ELEM_P2 0

@@ -38,7 +38,7 @@ class DistributedStepper(Stepper):
     with HODG_HALO=torch|host)."""
 
     def __init__(self, part: LocalPart, disc: Discretization, scheme="rk3", prec=_lib.PREC_F64, cfl=0.3,
-                 log_norms=True, group=None, halo="auto"):
+                 log_norms=True, group=None, halo="auto", use_graph=None):
         import os
 
         import torch
@@ -46,11 +46,18 @@ class DistributedStepper(Stepper):
 
         if halo == "auto":
             halo = os.environ.get("HODG_HALO", "native" if torch.device(disc.device).type == "cuda" else "torch")
-        # eager launches: the exchange and the reductions are stream-ordered
-        # (no host sync per step), so the host runs ahead of the GPU; NCCL
-        # point-to-point inside CUDA-graph capture is not used (a captured
-        # self-exchange hung on the B200 test box)
-        super().__init__(disc, scheme, prec, "global", cfl, log_norms=log_norms, use_graph=False, shadow=False)
+        # launches: eager by default -- the exchange and the reductions are
+        # stream-ordered (no host sync per step), so the host runs ahead of the
+        # GPU.  use_graph=True (or HODG_DIST_GRAPH=1) captures the whole step,
+        # NCCL exchange and all-reduces included, in one CUDA graph per dt
+        # parity (tools/scaling_estimate.py --capture measures both); the host
+        # halo never captures (it synchronises with the host).
+        if use_graph is None:
+            use_graph = os.environ.get("HODG_DIST_GRAPH", "0") == "1"
+        if halo == "host":
+            use_graph = False
+        super().__init__(disc, scheme, prec, "global", cfl, log_norms=log_norms, use_graph=use_graph,
+                         shadow=False)
         self.part = part
         self.group = group
         self.native = halo == "native"

@@ -1,30 +1,49 @@
-"""Per-rank compute of the partitioned C1M P2 step, measured on one GPU.
+"""Per-rank step time of the partitioned C1M P2 run, measured on one GPU
+through the shipped distributed schedule.
 
 Only one GPU is available to this build, so the strong-scaling run cannot be
-timed end to end.  This runs, for P = 1, 2, 4, 8 RCB parts, the exact local
-problem of the most loaded rank (owned elements + ghost rows, interior and
-partition faces) through the fused stepper on one GPU -- the ghost rows are
-filled once and not exchanged -- and reports its step time against t1 / P,
-plus the halo bytes per stage that the NCCL exchange moves while the
-interior-face kernel runs.
+timed end to end.  For P = 1, 2, 4, 8 RCB parts this takes the local problem
+of the most loaded rank (owned elements + ghost rows, interior and partition
+faces) and steps it with DistributedStepper exactly as bench.py --gpus P
+does -- per stage the NCCL halo exchange (pack kernel + grouped send / recv
+on the communication stream) posted before the interior-face kernel, the
+wait, the boundary + partition faces, the owned-element kernel; per step the
+dt MIN and norm SUM all-reduces -- over a 1-rank NCCL communicator whose rank
+is its own peer (tests/test_gpu_halo.py).  The halo therefore moves the
+rank's real ghost-row byte count, but as one device-local message instead
+of NVLink transfers to 3-7 peers; the NVLink time is added separately from
+the measured 770 GB/s peer bandwidth (B200_PROFILING.md) and is hidden
+behind the interior faces whenever it is shorter.
 
-usage: python tools/scaling_estimate.py [--n 55] [--steps 20]
+Reported per P: the eager schedule (the default, host-launched),
+optionally the same step captured in a CUDA graph (--capture), the
+compute-only graph-captured local step (no exchange), and the halo bytes per
+stage for ghost rows vs face traces (the alternative exchange north_star
+names).
+
+usage: python tools/scaling_estimate.py [--n 55] [--order 2] [--steps 20] [--capture]
 """
 import argparse
 import json
 import os
 import sys
+import types
 
 import numpy as np
 import torch
+import torch.distributed as dist
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
-import paper_2209_01877_b200 as P
-from paper_2209_01877_b200.dg import Discretization, _get_disc
-from paper_2209_01877_b200.geometry import compute_geometry
-from paper_2209_01877_b200.partition import build_local, rcb_partition
-from paper_2209_01877_b200.timestepping import Stepper
+import paper_2209_01877_b200 as P  # noqa: E402
+from paper_2209_01877_b200 import _lib  # noqa: E402
+from paper_2209_01877_b200.dg import Discretization, _get_disc  # noqa: E402
+from paper_2209_01877_b200.distributed import DistributedStepper  # noqa: E402
+from paper_2209_01877_b200.geometry import compute_geometry  # noqa: E402
+from paper_2209_01877_b200.partition import build_local, rcb_partition  # noqa: E402
+from paper_2209_01877_b200.timestepping import Stepper  # noqa: E402
+
+NVLINK_GBS = 770.0  # measured peer copy bandwidth per direction (B200_PROFILING.md)
 
 
 def time_steps(st, steps):
@@ -40,12 +59,26 @@ def time_steps(st, steps):
     return e0.elapsed_time(e1) / steps
 
 
+def self_plan(part):
+    """The rank's halo as one self-message of its real ghost-row count."""
+    sends = np.concatenate([np.asarray(part.send_idx[q], dtype=np.int64) for q in sorted(part.send_idx)])
+    ng = int(part.ghosts.size)
+    rows = np.resize(sends, ng).astype(np.int32)
+    return types.SimpleNamespace(send_idx={0: rows}, recv_range={0: (int(part.n_owned), ng)},
+                                 nparts=1, owned=part.owned)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=55)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--order", type=int, default=2)
+    ap.add_argument("--capture", action="store_true", help="also time the graph-captured distributed step")
     args = ap.parse_args()
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29531")
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1)
     bc = {"xmin": "far_field", "xmax": "far_field", "ymin": "far_field", "ymax": "far_field",
           "zmin": "slip_wall", "zmax": "slip_wall"}
     mesh = P.generate_tet_box(args.n, extent=(0.0, 0.0, 0.0, 10.0, 10.0, 10.0), bc=bc, device="cuda")
@@ -56,12 +89,13 @@ def main():
                             gas)
     full = _get_disc(mesh, geo, gas, bcs)
     rows_g = full.to_reference(st0.coeffs)
-    stepper = Stepper(full, "rk3", 64, "global", 0.3, use_graph=True)
+    stepper = Stepper(full, "rk3", _lib.PREC_F64, "global", 0.3, use_graph=True)
     stepper.load(st0)
     t1 = time_steps(stepper, args.steps)
+    print(f"P=1 {t1:.3f} ms", flush=True)
+    nqf, rs = full.nqf, full.rs
     out = [{"parts": 1, "owned": mesh.n_cells, "faces": mesh.n_faces, "step_ms": t1, "ideal_ms": t1,
-            "compute_efficiency": 1.0, "halo_rows": 0, "halo_mb_per_stage": 0.0}]
-    rs = full.rs
+            "efficiency": 1.0}]
     for nparts in (2, 4, 8):
         parts = rcb_partition(mesh.cell_centroid, nparts)
         counts = np.bincount(parts, minlength=nparts)
@@ -69,25 +103,44 @@ def main():
         part = build_local(mesh, parts, r)
         lgeo = compute_geometry(part.mesh, args.order, split=part.n_inner_faces)
         d = Discretization(part.mesh, lgeo, gas, bcs, n_elems=part.n_owned)
-        st = Stepper(d, "rk3", 64, "global", 0.3, use_graph=True)
-        # the DistributedStepper's schedule: boundary + partition faces after
-        # the interior ones (they wait for the halo), not on a side stream
-        st._side = None
         gl = torch.as_tensor(np.concatenate([part.owned, part.ghosts]), device="cuda")
-        st.A.copy_(rows_g.index_select(0, gl))
+        local_rows = rows_g.index_select(0, gl)
+        row = {"parts": nparts, "rank": r, "owned": int(part.n_owned), "ghosts": int(part.ghosts.size),
+               "faces": int(part.n_faces), "partition_faces": int(part.n_faces - part.n_inner_faces),
+               "ideal_ms": t1 / nparts}
+        # compute only: the local step in a CUDA graph, ghosts filled once
+        st = Stepper(d, "rk3", _lib.PREC_F64, "global", 0.3, use_graph=True)
+        st._side = None
+        st.A.copy_(local_rows)
         st.init_dt()
-        tp = time_steps(st, args.steps)
-        sent = sum(len(v) for v in part.send_idx.values())
-        out.append({"parts": nparts, "rank": r, "owned": int(part.n_owned), "ghosts": int(part.ghosts.size),
-                    "faces": int(part.n_faces), "partition_faces": int(part.n_faces - part.n_inner_faces),
-                    "step_ms": tp, "ideal_ms": t1 / nparts, "compute_efficiency": (t1 / nparts) / tp,
-                    "halo_rows": int(part.ghosts.size + sent),
-                    "halo_mb_per_stage": (part.ghosts.size + sent) * rs * 8 / 1e6})
+        row["compute_only_ms"] = time_steps(st, args.steps)
+        print(f"P={nparts} compute-only {row['compute_only_ms']:.3f} ms", flush=True)
+        del st
+        # the shipped schedule: DistributedStepper with the native NCCL halo
+        for mode in (["eager", "graph"] if args.capture else ["eager"]):
+            ds = DistributedStepper(self_plan(part), d, "rk3", _lib.PREC_F64, 0.3, log_norms=True,
+                                    halo="native", use_graph=(mode == "graph"))
+            ds.A.copy_(local_rows)
+            ds.init_dt()
+            print(f"P={nparts} {mode}: stepping", flush=True)
+            row[f"{mode}_ms"] = time_steps(ds, args.steps)
+            print(f"P={nparts} {mode} {row[f'{mode}_ms']:.3f} ms", flush=True)
+            ds.close()
+            del ds
+        # halo bytes per stage and direction: ghost rows (shipped) vs face traces
+        ghost_b = part.ghosts.size * rs * 8
+        trace_b = (part.n_faces - part.n_inner_faces) * nqf * 5 * 8
+        row["halo_mb_per_stage"] = {"ghost_rows": ghost_b / 1e6, "face_traces": trace_b / 1e6}
+        row["nvlink_us_per_stage"] = ghost_b / (NVLINK_GBS * 1e3)
+        best = min(row[k] for k in ("eager_ms", "graph_ms") if k in row)
+        row["efficiency"] = (t1 / nparts) / best
+        out.append(row)
     for row in out:
         print(json.dumps(row))
     os.makedirs("gpurun_out", exist_ok=True)
     with open(f"gpurun_out/scaling_estimate_n{args.n}_p{args.order}.json", "w") as fh:
         json.dump(out, fh, indent=1)
+    dist.destroy_process_group()
 
 
 if __name__ == "__main__":
