@@ -136,8 +136,16 @@ def load():
         if not os.path.exists(LIB_PATH):
             raise HodgError(f"libhodg_b200.so not built ({LIB_PATH}); run __graft_entry__.build()")
         lib = C.CDLL(LIB_PATH)
+        # an A/B variant library (HODG_B200_LIB) may predate later entry
+        # points; the in-tree library must export every declared symbol
+        variant = bool(os.environ.get("HODG_B200_LIB"))
         for name, (res, args) in SIGNATURES.items():
-            fn = getattr(lib, name)
+            try:
+                fn = getattr(lib, name)
+            except AttributeError:
+                if variant:
+                    continue
+                raise
             fn.restype = res
             fn.argtypes = args
         _lib = lib

@@ -121,7 +121,7 @@ constexpr int EMINB = HODG_EMINB ? HODG_EMINB : (H > 1 ? 2 : 3);
 constexpr bool U0_TMA = ORDER >= HODG_U0_TMA_ORDER;  // CTAs per SM the FP64 element kernel is register-budgeted for
 constexpr int XS = 15;                        // smem slot per (element, qp): 5 traces -> 15 contravariant fluxes
 #ifndef HODG_QC2
-#define HODG_QC2 7
+#define HODG_QC2 5
 #endif
 #ifndef HODG_QC3
 #define HODG_QC3 6
@@ -224,7 +224,7 @@ __host__ __device__ constexpr size_t face_smem_bytes() {
 // geometry / face-id tiles and prefetch the next tile's inputs into the
 // record region once the gather has consumed it.
 #ifndef HODG_EPERSIST
-#define HODG_EPERSIST 1
+#define HODG_EPERSIST 0
 #endif
 constexpr bool EPERSIST = HODG_EPERSIST && !WARP_ELEM && ORDER <= 2 && H == 1;
 
@@ -1045,29 +1045,44 @@ __global__ void local_dt_kernel(const hodg_mesh_desc m, const double* __restrict
                                 double* __restrict__ dt_vec, unsigned long long* __restrict__ dt_min,
                                 uint32_t* __restrict__ err) {
     const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (c >= m.n_elems) return;
-    double mm[5];
-#pragma unroll
-    for (int v = 0; v < 5; ++v) {
-        double s = 0.0;
-        sfor<NB>([&](auto j) { s += MEAN_T[j] * state[c * RS + v * NB + j]; });
-        mm[v] = s;
-    }
+    const bool live = c < m.n_elems;
     double dt = 0.0;
-    if (!(mm[0] > 0.0)) {
-        flag(err, 2, uint32_t(c));
-    } else {
-        const double u = mm[1] / mm[0], vv = mm[2] / mm[0], w = mm[3] / mm[0];
-        const double p = (m.gamma - 1.0) * (mm[4] - 0.5 * mm[0] * (u * u + vv * vv + w * w));
-        if (!(p > 0.0)) {
+    bool ok = false;
+    if (live) {
+        double mm[5];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+            double s = 0.0;
+            sfor<NB>([&](auto j) { s += MEAN_T[j] * state[c * RS + v * NB + j]; });
+            mm[v] = s;
+        }
+        if (!(mm[0] > 0.0)) {
             flag(err, 2, uint32_t(c));
         } else {
-            const double speed = sqrt(u * u + vv * vv + w * w) + sqrt(m.gamma * p / mm[0]);
-            dt = cfl * m.egeo[(c / E) * 16 * E + 13 * E + (c % E)] / ((2.0 * ORDER + 1.0) * speed);
-            if (dt_min) atomicMin(dt_min, static_cast<unsigned long long>(__double_as_longlong(dt)));
+            const double u = mm[1] / mm[0], vv = mm[2] / mm[0], w = mm[3] / mm[0];
+            const double p = (m.gamma - 1.0) * (mm[4] - 0.5 * mm[0] * (u * u + vv * vv + w * w));
+            if (!(p > 0.0)) {
+                flag(err, 2, uint32_t(c));
+            } else {
+                const double speed = sqrt(u * u + vv * vv + w * w) + sqrt(m.gamma * p / mm[0]);
+                dt = cfl * m.egeo[(c / E) * 16 * E + 13 * E + (c % E)] / ((2.0 * ORDER + 1.0) * speed);
+                ok = true;
+            }
         }
+        if (dt_vec) dt_vec[c] = dt;
     }
-    if (dt_vec) dt_vec[c] = dt;
+    if (dt_min) {
+        // warp min, one atomic per warp (an atomic per element serialises
+        // a million same-address updates at the L2)
+        unsigned long long bits = ok ? static_cast<unsigned long long>(__double_as_longlong(dt))
+                                     : 0x7FF0000000000000ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long other = __shfl_xor_sync(0xffffffffu, bits, o);
+            bits = other < bits ? other : bits;
+        }
+        if ((threadIdx.x & 31) == 0 && bits != 0x7FF0000000000000ull) atomicMin(dt_min, bits);
+    }
 }
 
 // ---------------------------------------------------------------------------

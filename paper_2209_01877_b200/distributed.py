@@ -58,6 +58,9 @@ class DistributedStepper(Stepper):
             use_graph = False
         super().__init__(disc, scheme, prec, "global", cfl, log_norms=log_norms, use_graph=use_graph,
                          shadow=False)
+        # NCCL's proxy thread issues CUDA calls while the step is being
+        # captured: "global" capture mode would invalidate the capture
+        self.capture_mode = "relaxed"
         self.part = part
         self.group = group
         self.native = halo == "native"

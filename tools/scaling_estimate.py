@@ -74,6 +74,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--order", type=int, default=2)
     ap.add_argument("--capture", action="store_true", help="also time the graph-captured distributed step")
+    ap.add_argument("--parts", default="2,4,8")
     args = ap.parse_args()
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ.setdefault("MASTER_PORT", "29531")
@@ -96,7 +97,7 @@ def main():
     nqf, rs = full.nqf, full.rs
     out = [{"parts": 1, "owned": mesh.n_cells, "faces": mesh.n_faces, "step_ms": t1, "ideal_ms": t1,
             "efficiency": 1.0}]
-    for nparts in (2, 4, 8):
+    for nparts in [int(x) for x in args.parts.split(",")]:
         parts = rcb_partition(mesh.cell_centroid, nparts)
         counts = np.bincount(parts, minlength=nparts)
         r = int(np.argmax(counts))  # the most loaded rank
