@@ -61,6 +61,7 @@ def parse():
     ap.add_argument("--layout", default="auto", choices=["auto", "elem", "face"], help="face flux record layout")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg (A/B runs)")
     ap.add_argument("--no-sub", action="store_true", help="skip the sub-records (A/B runs)")
+    ap.add_argument("--roofline-csv", default=None, help="also write the reference-format roofline CSV here")
     ap.add_argument("--partitioned", action="store_true",
                     help="use the partitioned (NCCL halo) stepper even at one rank")
     return ap.parse_args()
@@ -429,9 +430,24 @@ def run_ours(args):
                                         args.warmup, bw3, peaks)
         del m3, ge3, s3
         torch.cuda.empty_cache()
+        # config 4 on one GPU: the 8M-tet wedge-wing mesh, P2 (wall + far field)
+        wa = argparse.Namespace(**dict(vars(args), case="wing", n=110, order=2))
+        m4, g4, ge4, b4, s4, _ = build_case(wa)
+        sub["wing_c8m_p2_fp64"] = sub_record(f"config 4 wedge wing, n=110 ({m4.n_cells} tets), P2 FP64", m4, ge4, g4,
+                                             b4, s4, 2, 64, max(3, args.steps // 4), args.warmup, None, peaks)
+        del m4, ge4, s4
+        torch.cuda.empty_cache()
         line["sub"] = sub
     if rank == 0:
         line["cpu_baseline"] = None if (args.no_cpu or dist_mode) else cpu_baseline(args)
+        if args.roofline_csv:
+            # the reference's roofline CSV (hodg/perf.py:208-238) fed by this
+            # run's times, the algorithmic flops and the measured DRAM bytes
+            samples = [("c1m_stage_alg_bytes", PF.PerfSample(stage_s, flops_stage, alg, 1))]
+            if traffic:
+                samples.append(("c1m_stage_ncu_bytes", PF.PerfSample(stage_s, flops_stage, float(traffic), 1)))
+            machine = PF.MachineModel("b200-measured", PF.FP64_FLOPS_PER_S, peaks["hbm_gbs"] * 1e9)
+            PF.emit_roofline_csv(samples, [machine], args.roofline_csv)
         print(json.dumps(line), flush=True)
     if dist_mode:
         torch.cuda.synchronize()

@@ -237,7 +237,7 @@ struct ElemSmem {
     static constexpr size_t htile = align16(fid + size_t(NGB) * 4 * E * 4);  // state tile, then the records
     static constexpr size_t hrec = ES ? size_t(E) * EREC * sizeof(T) : size_t(4) * E * hsmem<T>() * sizeof(T);
     static constexpr size_t sbytes = size_t(E) * RS * 8;
-    static constexpr size_t hbytes = cmax(hrec, sbytes);
+    static constexpr size_t hbytes = EPERSIST ? cmax(hrec, sbytes) : hrec;
     static constexpr size_t sx = align16(htile + hbytes);
     static constexpr size_t red = sx + sbytes;                               // (5 + 5H) x E doubles
     static constexpr size_t s32 = red + size_t(5 + 5 * H) * E * 8;           // mixed: FP32 output tile
@@ -277,19 +277,28 @@ __device__ __forceinline__ void hsel(int h, F&& f) {
 // two (refelem.py builds the tables as products).  Only the c = 0 monomials
 // are contracted (P2: 6 of 10, P3: 10 of 20); the rest are one scaling each
 // and equal the direct contraction bit for bit.
-template <typename T, int S, int I0, int N, int NQ>
+#ifndef HODG_FOLD
+#define HODG_FOLD 1
+#endif
+template <typename T, int S0, int I0, int N, int NQ>
 __device__ __forceinline__ void face_moments(const T (&hq)[NQ], T (&fa)[N]) {
+    constexpr int S = S0;
+    constexpr bool FOLD = HODG_FOLD && !(HODG_FOLD == 2 && N != NB);  // 2: only without a basis split
     constexpr int d = S - 1;
+    auto direct = [](auto i) {
+        return !FOLD || S == 0 || expt(I0 + decltype(i)::value, d < 0 ? 0 : d) == 0;
+    };
+    // points outer, basis inner: consecutive table entries pair into 128-bit
+    // constant loads (LDCU.128)
     sfor<N>([&](auto i) {
-        constexpr int ig = I0 + i;
-        constexpr bool direct = S == 0 || expt(ig, d < 0 ? 0 : d) == 0;
-        if constexpr (direct) {
-            T x = T(0);
-            sfor<NQ>([&](auto q) { x += TAB(FG, T, (S * NQ + q) * NB + ig) * hq[q]; });
-            fa[i] = x;
-        }
+        if constexpr (direct(i)) fa[i] = T(0);
     });
-    if constexpr (S > 0) {
+    sfor<NQ>([&](auto q) {
+        sfor<N>([&](auto i) {
+            if constexpr (direct(i)) fa[i] += TAB(FG, T, (S * NQ + q) * NB + I0 + i) * hq[q];
+        });
+    });
+    if constexpr (FOLD && S > 0) {
         sfor<N>([&](auto i) {
             constexpr int ig = I0 + i;
             constexpr int c = expt(ig, d);
@@ -304,7 +313,7 @@ __device__ __forceinline__ void face_moments(const T (&hq)[NQ], T (&fa)[N]) {
                     // basis split: the base function lives in the other part
                     T x = T(0);
                     sfor<NQ>([&](auto q) { x += TAB(FG, T, (S * NQ + q) * NB + ig) * hq[q]; });
-                    fa[i] = x;
+                    fa[i] = x;  // (rare: only with H > 1)
                 }
             }
         });
@@ -586,7 +595,10 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : 4) : E
     extern __shared__ __align__(16) unsigned char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::bar);  // [0, 1] inputs per buffer, [2] records, [3] u0
     T* HT = reinterpret_cast<T*>(smem + L::htile);
-    double* SIN = reinterpret_cast<double*>(smem + L::htile);    // the state tile, before the records land
+    // the state tile: in the record region when persistent (the next tile's
+    // prefetch lands there), else in the X region, so the element-slot
+    // records can be fetched at once, alongside it
+    double* SIN = reinterpret_cast<double*>(smem + (EPERSIST ? L::htile : L::sx));
     double* Z = reinterpret_cast<double*>(smem + L::htile);      // H > 1: residual exchange (after the gather)
     double* S = reinterpret_cast<double*>(smem + L::sx);         // u0 tile, then the output tile
     T* X = reinterpret_cast<T*>(smem + L::sx);                   // per-chunk trace / flux slots
@@ -623,10 +635,20 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : 4) : E
         mbar_fence_init();
         if (tile < ntiles) issue_inputs(tile, 0);  // the stage state: two launches back
     }
-    __syncthreads();
     // programmatic dependent launch: everything above overlapped the face
     // kernel's tail; records, and the in-place output, need it complete
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    if constexpr (ES && !EPERSIST) {
+        // element-slot records: one bulk copy, in flight with the state tile
+        if (t == 0 && tile < ntiles) {
+            const int64_t e0 = tile * E;
+            const int ne = int(min(int64_t(E), m.n_elems - e0));
+            const uint32_t hb = uint32_t(align16(size_t(ne) * EREC * sizeof(T)));
+            mbar_arrive_expect_tx(bar + 2, hb);
+            bulk_g2s(HT, hbuf + e0 * EREC, hb, bar + 2);
+        }
+    }
+    __syncthreads();
     asm volatile("griddepcontrol.launch_dependents;");
 
     for (int it = 0; tile < ntiles; tile += gridDim.x, ++it) {
@@ -659,10 +681,12 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : 4) : E
                 }
             }
         }
-        __syncthreads();  // state tile consumed: the region receives the face flux records
+        __syncthreads();  // state tile consumed (persistent: the region receives the records)
 
         // face flux records, in flight during the volume integral
-        if constexpr (ES) {
+        if constexpr (ES && !EPERSIST) {
+            // issued at kernel start, with the state tile
+        } else if constexpr (ES) {
             if (t == 0 && ne > 0) {
                 const uint32_t hb = uint32_t(align16(size_t(ne) * EREC * sizeof(T)));
                 fence_proxy_async();

@@ -136,6 +136,13 @@ class DistributedStepper(Stepper):
     def close(self):
         """Release the exchange (the native one owns an NCCL communicator);
         call before destroying the process group."""
+        import torch
+
+        # captured steps hold NCCL work: drop the graphs before the
+        # communicator (destroying it under a live graph exec blocks)
+        self._graphs.clear()
+        self._args.clear()
+        torch.cuda.synchronize()
         close = getattr(self.halo, "close", None)
         if close is not None:
             close()

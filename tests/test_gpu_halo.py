@@ -108,9 +108,13 @@ def test_two_partitions_through_the_native_exchange(P):
         assert torch.equal(res[: part.n_owned], ref.index_select(0, own)), r
 
 
-def test_distributed_stepper_native_halo_single_rank(P):
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("use_graph", [False, True])
+def test_distributed_stepper_native_halo_single_rank(P, use_graph):
     """DistributedStepper on a 1-rank NCCL group with the native exchange (no
-    peers): same states as the single-GPU stepper."""
+    peers): same states as the single-GPU stepper -- launched eagerly, and
+    captured in a CUDA graph with the NCCL all-reduces inside (relaxed
+    capture mode; close() drops the graphs before the communicator)."""
     import socket
 
     import torch
@@ -133,18 +137,19 @@ def test_distributed_stepper_native_halo_single_rank(P):
         _, c = oracle_state(m, 1)
         st0 = P.DofState(torch.from_numpy(c).cuda())
         part, disc = setup_partitioned(m, 1, gas, bcs, 0, 1)
-        ds = DistributedStepper(part, disc, "rk3", 64, 0.3, log_norms=True, halo="native")
+        ds = DistributedStepper(part, disc, "rk3", 64, 0.3, log_norms=True, halo="native", use_graph=use_graph)
         ds.load(owned_state(st0, part))
         ref = Stepper(_get_disc(m, geo, gas, bcs), "rk3", 64, "global", 0.3, use_graph=False)
         ref.load(st0)
-        for _ in range(2):
+        for _ in range(3):
             ds.step()
             ref.step()
         ds.check()
         ref.check()
         own = torch.as_tensor(part.owned, device="cuda")
         assert torch.equal(ds.state().coeffs, ref.state().coeffs.index_select(0, own))
-        ds.halo.close()
+        assert torch.allclose(ds.norms, ref.norms, rtol=1e-12, atol=0)  # (summation order differs)
+        ds.close()
     finally:
         dist.destroy_process_group()
 
