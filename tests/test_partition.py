@@ -205,3 +205,50 @@ def test_partitioned_rk3_equals_serial_bitwise(world):
     for _, owned, rows in results:
         got[owned] = rows
     assert np.array_equal(got, u)
+
+
+def _host_halo_main(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2209_01877_b200.partition import HostHaloExchange
+
+    m = box()
+    parts = rcb_partition(m.cell_centroid, world)
+    part = build_local(m, parts, rank)
+    # rows = global id encoded in every column; ghosts start as NaN
+    gl = np.concatenate([part.owned, part.ghosts])
+    rows = torch.full((part.n_rows, 7), float("nan"), dtype=torch.float64)
+    rows[: part.n_owned] = torch.from_numpy(np.repeat(part.owned[:, None].astype(np.float64), 7, axis=1))
+    h = HostHaloExchange(part, "cpu")
+    h.start(rows)
+    h.wait()
+    dt = torch.tensor([float(rank + 3)], dtype=torch.float64).view(torch.int64)
+    h.allreduce(dt, 0)
+    s = torch.tensor([1.0 + rank], dtype=torch.float64)
+    h.allreduce(s, 1)
+    out_q.put((rank, np.array_equal(rows.numpy(), np.repeat(gl[:, None].astype(np.float64), 7, axis=1)),
+               float(dt.view(torch.float64).item()), float(s.item())))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_host_staged_halo_exchange(world):
+    """HostHaloExchange (the transport of tests/test_gpu_multirank.py) over
+    gloo: every ghost row arrives from its owner, the dt MIN and norm SUM
+    reductions are exact."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_host_halo_main, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for rank, ok, dtmin, ssum in res:
+        assert ok, rank
+        assert dtmin == 3.0
+        assert ssum == sum(1.0 + r for r in range(world))
