@@ -14,7 +14,17 @@
 
 #define HODG_CAT_(a, b) a##b
 #define HODG_CAT(a, b) HODG_CAT_(a, b)
-#define TAB(NAME, T, k) (sizeof(T) == 8 ? (T)HODG_CAT(NAME, _D)[(k)] : (T)HODG_CAT(NAME, _F)[(k)])
+// FP32 tables as compile-time constants (each value an FFMA immediate) or
+// as __constant__ arrays (a uniform-register load per 4 values)
+#ifndef HODG_F32_IMM
+#define HODG_F32_IMM 1
+#endif
+#if HODG_F32_IMM
+#define HODG_TABF(NAME) HODG_CAT(NAME, _FX)
+#else
+#define HODG_TABF(NAME) HODG_CAT(NAME, _F)
+#endif
+#define TAB(NAME, T, k) (sizeof(T) == 8 ? (T)HODG_CAT(NAME, _D)[(k)] : (T)HODG_TABF(NAME)[(k)])
 
 namespace hodg {
 namespace HODG_CAT(ord, ORDER) {
