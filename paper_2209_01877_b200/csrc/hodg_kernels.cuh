@@ -52,6 +52,9 @@ constexpr int FACE_THREADS = 128;
 #ifndef HODG_ROE_PAIRS
 #define HODG_ROE_PAIRS 1
 #endif
+#ifndef HODG_FACE_MINB_F
+#define HODG_FACE_MINB_F 6  // mixed-precision face kernel: CTAs per SM of the register budget (80 registers)
+#endif
 #ifndef HODG_FACE_MINB
 #define HODG_FACE_MINB 4
 #endif
@@ -124,21 +127,29 @@ inline int64_t hodg_pdl_max_elems() {
 #define HODG_EMINB 0
 #endif
 // CTAs per SM the FP64 element kernel is register-budgeted for
-constexpr int EMINB = HODG_EMINB ? HODG_EMINB : (H > 1 ? 2 : 3);
+// (P2 FP64: 4 CTAs -- 96 registers and, with 4 volume points per chunk and
+// unpadded record rows, 56.9 KB of shared memory: 20 warps per SM instead of 15)
+constexpr int EMINB = HODG_EMINB ? HODG_EMINB : (H > 1 ? 2 : (ORDER == 2 ? 4 : 3));
 #ifndef HODG_U0_TMA_ORDER
 #define HODG_U0_TMA_ORDER 0  // orders >= this fetch u0 by TMA after the volume phases (else: registers)
 #endif
 constexpr bool U0_TMA = ORDER >= HODG_U0_TMA_ORDER;  // CTAs per SM the FP64 element kernel is register-budgeted for
 constexpr int XS = 15;                        // smem slot per (element, qp): 5 traces -> 15 contravariant fluxes
+#ifndef HODG_QC2F
+#define HODG_QC2F 5  // P2 mixed precision
+#endif
 #ifndef HODG_QC2
-#define HODG_QC2 5
+#define HODG_QC2 4
 #endif
 #ifndef HODG_QC3
 #define HODG_QC3 6
 #endif
 // volume qps per chunk (bounds the X buffer; at P3 small enough for 4 CTAs/SM)
-constexpr int QC = (NQV <= 8) ? NQV : (ORDER == 2 ? HODG_QC2 : HODG_QC3);
-constexpr int NCH = (NQV + QC - 1) / QC;
+// volume points per chunk of the element kernel, per arithmetic type
+template <typename T>
+__host__ __device__ constexpr int qc() {
+    return (NQV <= 8) ? NQV : (ORDER == 2 ? (sizeof(T) == 8 ? HODG_QC2 : HODG_QC2F) : HODG_QC3);
+}
 
 // padded per-face record of the face flux buffer: 5 x NQF values rounded up
 // to 16 bytes so each face is one TMA bulk copy
@@ -146,9 +157,15 @@ template <typename T>
 __host__ __device__ constexpr int hstride() {
     return int(((5 * NQF * sizeof(T) + 15) / 16) * 16 / sizeof(T));
 }
-// smem stride of the gathered face records (2-way worst-case bank pattern)
+// smem stride of the gathered face records: padded for the bank pattern,
+// except at P2 where the unpadded rows let 4 FP64 element CTAs fit an SM
+#ifndef HODG_HSS_NOPAD
+#define HODG_HSS_NOPAD (ORDER == 2)
+#endif
+constexpr bool HSS_NOPAD = HODG_HSS_NOPAD;
 template <typename T>
 __host__ __device__ constexpr int hsmem() {
+    if (HSS_NOPAD) return hstride<T>();
     return sizeof(T) == 8 ? ((hstride<T>() % 4 == 2) ? hstride<T>() : hstride<T>() + 2) : hstride<T>();
 }
 
@@ -253,7 +270,7 @@ struct ElemSmem {
     static constexpr size_t s32 = red + size_t(5 + 5 * H) * E * 8;           // mixed: FP32 output tile
     static constexpr size_t s32_bytes = sizeof(T) == 4 ? size_t(E) * RSF * 4 : 0;
     static constexpr size_t sx_bytes =
-        cmax(sbytes + size_t(5 + 5 * H) * E * 8 + s32_bytes, size_t(QC) * E * XS * sizeof(T));
+        cmax(sbytes + size_t(5 + 5 * H) * E * 8 + s32_bytes, size_t(qc<T>()) * E * XS * sizeof(T));
     static constexpr size_t total = sx + sx_bytes;
     // H > 1: the residual exchange of the mass solve reuses the record tile
     static_assert(H == 1 || hbytes >= size_t(5) * E * NB * 8, "solve exchange fits the record tile");
@@ -344,7 +361,8 @@ __device__ __forceinline__ void face_moments(const T (&hq)[NQ], T (&fa)[N]) {
 //  record is stored in the blocks of both (owned) neighbours, so the element
 //  kernel fetches a tile's records with one contiguous copy.
 template <typename T, bool BND, bool ES, typename R = double>
-__global__ void __launch_bounds__(FACE_THREADS, HODG_FACE_MINB) face_flux_kernel(const hodg_mesh_desc m,
+__global__ void __launch_bounds__(FACE_THREADS, sizeof(T) == 4 ? HODG_FACE_MINB_F : HODG_FACE_MINB)
+    face_flux_kernel(const hodg_mesh_desc m,
                                                                     const R* __restrict__ state,
                                                                     T* __restrict__ hbuf,
                                                                     uint32_t* __restrict__ err, int64_t f_begin,
@@ -595,8 +613,11 @@ __global__ void __launch_bounds__(FACE_THREADS, HODG_FACE_MINB) face_flux_kernel
 // the hot phases is unit-stride across the warp.
 // ES: the records are in the element-slot layout -- one bulk copy of the
 // tile's record blocks, issued with the state tile, no per-face gather.
+#ifndef HODG_EMINB_F
+#define HODG_EMINB_F 5  // mixed-precision element kernel at P0-P2 (72 registers)
+#endif
 template <typename T, bool ES>
-__global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : 4) : EMINB)
+__global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : HODG_EMINB_F) : EMINB)
     elem_stage_kernel(const hodg_mesh_desc m, const T* __restrict__ hbuf, const hodg_stage_args a,
                       uint32_t* __restrict__ err) {
     using L = ElemSmem<T, ES>;
@@ -743,6 +764,8 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : 4) : E
 #pragma unroll
             for (int k = 0; k < 9; ++k) ji[k] = T(G[k * E + e]);
         }
+        constexpr int QC = qc<T>();
+        constexpr int NCH = (NQV + QC - 1) / QC;
         sfor<NCH>([&](auto ch) {
             constexpr int q0 = ch * QC;
             constexpr int nq = (NQV - q0) < QC ? (NQV - q0) : QC;
