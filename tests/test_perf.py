@@ -49,3 +49,17 @@ def test_roofline_attainable():
     mm = perf.MachineModel("x", 10.0, 2.0)
     assert perf.roofline_attainable(mm, 1.0) == 2.0
     assert perf.roofline_attainable(mm, 100.0) == 10.0
+
+
+def test_algorithmic_flops_reference_convention():
+    """~16.8k flops per element per stage at C1M P2 in the
+    reference's convention (add / mul / div / sqrt = 1), independent of the
+    kernels; P1 < P2 < P3 per element."""
+    from paper_2209_01877_b200 import perf
+
+    n, f, fb = 998250, 2014650, 36300
+    per = {p: perf.algorithmic_flops_per_stage(n, f, fb, p) / n for p in (1, 2, 3)}
+    assert 16500 < per[2] < 17200
+    assert per[1] < per[2] < per[3]
+    # rk2 stages carry fewer RK flops per DOF than rk3 stages
+    assert perf.algorithmic_flops_per_stage(n, f, fb, 2, "rk2") > 0
