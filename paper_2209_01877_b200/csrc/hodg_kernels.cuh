@@ -56,7 +56,7 @@ constexpr int FACE_THREADS = 128;
 #define HODG_FACE_MINB_F 6  // mixed-precision face kernel: CTAs per SM of the register budget (80 registers)
 #endif
 #ifndef HODG_FACE_MINB
-#define HODG_FACE_MINB 4
+#define HODG_FACE_MINB (ORDER == 3 ? 5 : 4)
 #endif
 #ifndef HODG_ELEM_CPASYNC
 #define HODG_ELEM_CPASYNC 0  // CTA element kernel: face records by cp.async chunks (0: one TMA copy per record; faster)
@@ -237,10 +237,19 @@ __host__ __device__ constexpr int expt(int i, int d) {
 
 // R: element type of the state rows the face kernel reads -- the FP64 state,
 // or (mixed precision) its FP32 shadow
+// row buffers of the face kernel: 2 (the next tile's rows stream in during
+// this tile's Riemann phase) or 1 (less shared memory: more CTAs per SM,
+// the next tile's copies issued after the Riemann phase)
+// (P3: one buffer at 5 CTAs per SM, 94 registers, measured 4.5% faster;
+// P1 / P2: two buffers at 4 CTAs)
+#ifndef HODG_FACE_NBUF
+#define HODG_FACE_NBUF (ORDER == 3 ? 1 : 2)
+#endif
+constexpr int FNBUF = HODG_FACE_NBUF;
 template <typename T, typename R = double>
 __host__ __device__ constexpr size_t face_smem_bytes() {
     return align16(16 + 4 * FBS * sizeof(T)) +
-           2 * align16(cmax(size_t(2 * FT) * rstride<R>() * sizeof(R), size_t(2 * FT) * NQF * 5 * sizeof(T)));
+           FNBUF * align16(cmax(size_t(2 * FT) * rstride<R>() * sizeof(R), size_t(2 * FT) * NQF * 5 * sizeof(T)));
 }
 
 // element kernel shared memory carve-up
@@ -473,11 +482,11 @@ __global__ void __launch_bounds__(FACE_THREADS, sizeof(T) == 4 ? HODG_FACE_MINB_
     if (tile < ntiles) publish(cur, 0);
     const T gam = T(m.gamma);
     for (int it = 0; tile < ntiles; tile += gridDim.x, ++it) {
-        const int buf = it & 1;
+        const int buf = FNBUF == 2 ? (it & 1) : 0;
         const int64_t f0 = f_begin + int64_t(tile) * FT;
         const int nf = int(min(int64_t(FT), f_end - f0));
         const Meta nxt = load_meta(tile + gridDim.x);  // in flight during this tile
-        mbar_wait(bar + buf, (it >> 1) & 1);
+        mbar_wait(bar + buf, FNBUF == 2 ? ((it >> 1) & 1) : (it & 1));
 
         // phase 1: traces of this side at qps [g*QPT, g*QPT + QPT)
         const R* myrow = rows0 + buf * BUF + size_t(side * FT + lf) * RR;
@@ -518,7 +527,7 @@ __global__ void __launch_bounds__(FACE_THREADS, sizeof(T) == 4 ? HODG_FACE_MINB_
             }
         }
         // next tile: its rows stream into the other buffer during phase 2
-        if (tile + gridDim.x < ntiles) publish(nxt, buf ^ 1);
+        if (FNBUF == 2 && tile + gridDim.x < ntiles) publish(nxt, buf ^ 1);
         __syncthreads();
 
         // phase 2: Riemann flux at each (face, qp); two pairs per thread per
@@ -591,6 +600,11 @@ __global__ void __launch_bounds__(FACE_THREADS, sizeof(T) == 4 ? HODG_FACE_MINB_
                     for (int v = 0; v < 5; ++v) hbuf[fid[k] * HS + v * NQF + qv[k]] = h[k][v];
                 }
             }
+        }
+        if constexpr (FNBUF == 1) {
+            // single buffer: the traces and this tile's metadata are consumed
+            __syncthreads();
+            if (tile + gridDim.x < ntiles) publish(nxt, 0);
         }
         cur = nxt;
     }
