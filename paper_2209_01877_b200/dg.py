@@ -350,12 +350,17 @@ def project_initial(mesh: TetMesh, geo: DeviceGeometry, field, gas: GasModel, de
                         for a in (w.rho, w.u, w.v, w.w, w.p))
     if np.any(rho <= 0.0) or np.any(p <= 0.0):
         raise AdmissibilityError("initial field is inadmissible")
-    e = p / (gas.gamma - 1.0) + 0.5 * rho * (u * u + v * v + ww * ww)
-    q = np.stack([rho, rho * u, rho * v, rho * ww, e], axis=-1)  # (n, nqv, 5)
-    ref = np.einsum("iq,nqv->nvi", t.projector, q)  # (n, 5, nb) reference basis
     disc = _get_disc(mesh, geo, gas, BoundaryConditions(Conserved(1.0, 0.0, 0.0, 0.0, 1.0)))
+    # conserved variables and the projection on the device (the callback is
+    # the reference's host API; the rest is one batched contraction)
+    dev = disc.device
+    rho_d, u_d, v_d, w_d, p_d = (torch.from_numpy(np.array(a, dtype=np.float64)).to(dev) for a in (rho, u, v, ww, p))
+    e = p_d / (gas.gamma - 1.0) + 0.5 * rho_d * (u_d * u_d + v_d * v_d + w_d * w_d)
+    q = torch.stack([rho_d, rho_d * u_d, rho_d * v_d, rho_d * w_d, e], dim=-1)  # (n, nqv, 5)
+    proj = torch.from_numpy(t.projector).to(dev)
+    ref = torch.einsum("iq,nqv->nvi", proj, q)  # (n, 5, nb) reference basis
     rows = disc.new_state()
-    rows[: mesh.n_cells, : N_VARS * t.nb] = torch.from_numpy(ref.reshape(mesh.n_cells, -1)).to(disc.device)
+    rows[: mesh.n_cells, : N_VARS * t.nb] = ref.reshape(mesh.n_cells, -1)
     return DofState(disc.from_reference(rows))
 
 
