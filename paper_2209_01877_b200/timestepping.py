@@ -288,10 +288,11 @@ class Stepper:
     def _records(self, prec):
         """Face flux record buffer: the element-slot layout (one bulk copy per
         element tile, but two record stores per face) or the face-ordered one.
-        "auto" takes the faster on the B200: element-slot for
-        mixed precision and at P3, face-ordered for FP64 at P0-P2."""
-        use_elem = self.layout == "elem" or (
-            self.layout == "auto" and (prec == _lib.PREC_MIXED or self.disc.order >= 3))
+        "auto" takes the faster on the B200: element-slot at P3,
+        face-ordered at P0-P2 in both precisions (round 2: with the FP32 shadow
+        and 6 mixed face CTAs per SM the face kernel's second record store
+        costs more than the element kernel's per-record copies save)."""
+        use_elem = self.layout == "elem" or (self.layout == "auto" and self.disc.order >= 3)
         return self.disc.elem_buffer(prec) if use_elem else self.disc.face_buffer(prec)
 
     def _stage_args(self, k, parity):
