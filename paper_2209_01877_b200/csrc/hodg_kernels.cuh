@@ -56,7 +56,7 @@ constexpr int FACE_THREADS = 128;
 #define HODG_FACE_MINB_F 6  // mixed-precision face kernel: CTAs per SM of the register budget (80 registers)
 #endif
 #ifndef HODG_FACE_MINB
-#define HODG_FACE_MINB (ORDER == 3 ? 5 : 4)
+#define HODG_FACE_MINB (ORDER == 2 ? 4 : 5)
 #endif
 #ifndef HODG_ELEM_CPASYNC
 #define HODG_ELEM_CPASYNC 0  // CTA element kernel: face records by cp.async chunks (0: one TMA copy per record; faster)
@@ -165,8 +165,11 @@ __host__ __device__ constexpr int hstride() {
 constexpr bool HSS_NOPAD = HODG_HSS_NOPAD;
 template <typename T>
 __host__ __device__ constexpr int hsmem() {
+    // FP32: a stride that is a multiple of 32 words would put every element
+    // of a warp on one bank; +4 words keeps 16-byte alignment (4-way at most)
+    if (sizeof(T) == 4) return hstride<T>() % 32 == 0 ? hstride<T>() + 4 : hstride<T>();
     if (HSS_NOPAD) return hstride<T>();
-    return sizeof(T) == 8 ? ((hstride<T>() % 4 == 2) ? hstride<T>() : hstride<T>() + 2) : hstride<T>();
+    return (hstride<T>() % 4 == 2) ? hstride<T>() : hstride<T>() + 2;
 }
 
 // element-slot record block: the 4 face records of an element (5 x NQF
@@ -263,6 +266,9 @@ __host__ __device__ constexpr size_t face_smem_bytes() {
 #define HODG_EPERSIST 0
 #endif
 constexpr bool EPERSIST = HODG_EPERSIST && !WARP_ELEM && ORDER <= 2 && H == 1;
+#ifndef HODG_RED_HT
+#define HODG_RED_HT 1
+#endif
 
 template <typename T, bool ES>
 struct ElemSmem {
@@ -275,11 +281,17 @@ struct ElemSmem {
     static constexpr size_t sbytes = size_t(E) * RS * 8;
     static constexpr size_t hbytes = EPERSIST ? cmax(hrec, sbytes) : hrec;
     static constexpr size_t sx = align16(htile + hbytes);
-    static constexpr size_t red = sx + sbytes;                               // (5 + 5H) x E doubles
-    static constexpr size_t s32 = red + size_t(5 + 5 * H) * E * 8;           // mixed: FP32 output tile
     static constexpr size_t s32_bytes = sizeof(T) == 4 ? size_t(E) * RSF * 4 : 0;
-    static constexpr size_t sx_bytes =
-        cmax(sbytes + size_t(5 + 5 * H) * E * 8 + s32_bytes, size_t(qc<T>()) * E * XS * sizeof(T));
+    static constexpr size_t red_bytes = size_t(5 + 5 * H) * E * 8;
+    // mixed precision: the reduction slots and the FP32 output tile reuse the
+    // record region once the gather has consumed it (one barrier), so a CTA
+    // is the records + max(state / output tile, X) only
+    static constexpr bool rht =
+        HODG_RED_HT && sizeof(T) == 4 && H == 1 && !EPERSIST && red_bytes + s32_bytes <= hbytes;
+    static constexpr size_t red = rht ? htile : sx + sbytes;                 // (5 + 5H) x E doubles
+    static constexpr size_t s32 = red + red_bytes;                           // mixed: FP32 output tile
+    static constexpr size_t sx_bytes = rht ? cmax(sbytes, size_t(qc<T>()) * E * XS * sizeof(T))
+                                           : cmax(sbytes + red_bytes + s32_bytes, size_t(qc<T>()) * E * XS * sizeof(T));
     static constexpr size_t total = sx + sx_bytes;
     // H > 1: the residual exchange of the mass solve reuses the record tile
     static_assert(H == 1 || hbytes >= size_t(5) * E * NB * 8, "solve exchange fits the record tile");
@@ -628,7 +640,7 @@ __global__ void __launch_bounds__(FACE_THREADS, sizeof(T) == 4 ? HODG_FACE_MINB_
 // ES: the records are in the element-slot layout -- one bulk copy of the
 // tile's record blocks, issued with the state tile, no per-face gather.
 #ifndef HODG_EMINB_F
-#define HODG_EMINB_F 5  // mixed-precision element kernel at P0-P2 (72 registers)
+#define HODG_EMINB_F 6  // mixed-precision element kernel at P0-P2 (64 registers; RED / FP32 tile in the record region)
 #endif
 template <typename T, bool ES>
 __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : HODG_EMINB_F) : EMINB)
@@ -963,6 +975,7 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : HODG_E
                 for (int k = 0; k < NB; ++k) full[k] = Z[(v * E + e) * NB + k];
             }
         }
+        if constexpr (L::rht) __syncthreads();  // records consumed: the region takes RED / the FP32 tile
         if constexpr (EPERSIST) {
             // the records are consumed: the next tile's inputs stream into the
             // region during this tile's solve and epilogue

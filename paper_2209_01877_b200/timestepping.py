@@ -288,11 +288,12 @@ class Stepper:
     def _records(self, prec):
         """Face flux record buffer: the element-slot layout (one bulk copy per
         element tile, but two record stores per face) or the face-ordered one.
-        "auto" takes the faster on the B200: element-slot at P3,
-        face-ordered at P0-P2 in both precisions (round 2: with the FP32 shadow
-        and 6 mixed face CTAs per SM the face kernel's second record store
-        costs more than the element kernel's per-record copies save)."""
-        use_elem = self.layout == "elem" or (self.layout == "auto" and self.disc.order >= 3)
+        "auto" takes the faster on the B200: element-slot at P3
+        and for mixed precision at P0, face-ordered otherwise (round 2, C1M:
+        mixed P1 4.65e10 face vs 4.28e10 element-slot, P2 7.51e10 vs 7.40e10,
+        P0 2.34e10 vs 2.53e10)."""
+        use_elem = self.layout == "elem" or (
+            self.layout == "auto" and (self.disc.order >= 3 or (prec == _lib.PREC_MIXED and self.disc.order == 0)))
         return self.disc.elem_buffer(prec) if use_elem else self.disc.face_buffer(prec)
 
     def _stage_args(self, k, parity):
