@@ -11,7 +11,9 @@
 // to stage element tiles in shared memory.
 #pragma once
 
+#include <cuda.h>  // CUtensorMap (encoded through the runtime's driver entry point; no libcuda link)
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 #include <stdint.h>
 
 #include "../../include/hodg_b200.h"
@@ -68,6 +70,46 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
             smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
+}
+
+// four rows of a 2-D tensor map (row indices r0..r3; out-of-range rows, e.g.
+// -1, are zero-filled without a memory read) -> four consecutive rows at dst
+// (128-byte aligned), completion counted on `bar`: one instruction where
+// per-row bulk copies take four (sm_100 tile::gather4)
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* tm, int r0, int r1, int r2, int r3,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+        "l"(tm), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// host: the 2-D row map of a row array (rows of `cols` elements, 8- or
+// 4-byte, `cols * elem` a multiple of 16 bytes) for tma_gather4: box = one
+// full row.  The row count is left open (2^31 - 1): the kernels index only
+// valid rows or -1.
+#ifndef HODG_G4_PROMOTION
+#define HODG_G4_PROMOTION CU_TENSOR_MAP_L2_PROMOTION_NONE
+#endif
+static inline int encode_row_map(CUtensorMap* tm, const void* base, int cols, int elem_bytes) {
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    if (!enc) {
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&enc), cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !enc)
+            return HODG_ECUDA;
+    }
+    const cuuint64_t gdim[2] = {cuuint64_t(cols), cuuint64_t(0x7FFFFFFF)};
+    const cuuint64_t gstride[1] = {cuuint64_t(cols) * elem_bytes};
+    const cuuint32_t box[2] = {cuuint32_t(cols), 1};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult r = enc(tm, elem_bytes == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                           const_cast<void*>(base), gdim, gstride, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_NONE, HODG_G4_PROMOTION,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? HODG_OK : HODG_ECUDA;
 }
 
 // shared -> global (bulk group); caller waits with bulk_wait_read()

@@ -249,10 +249,28 @@ __host__ __device__ constexpr int expt(int i, int d) {
 #define HODG_FACE_NBUF (ORDER == 3 ? 1 : 2)
 #endif
 constexpr int FNBUF = HODG_FACE_NBUF;
+// state rows by TMA tile::gather4: four (face, side) rows per instruction
+// (one per row otherwise); rows land in 128-byte-aligned groups of four
+#ifndef HODG_FACE_G4
+#define HODG_FACE_G4 1
+#endif
+constexpr bool FG4 = HODG_FACE_G4 && !HODG_FACE_CPASYNC;
+template <typename R>
+__host__ __device__ constexpr int g4_stride() {  // elements per group of four rows
+    return int((4 * rstride<R>() * sizeof(R) + 127) / 128 * 128 / sizeof(R));
+}
+// smem offset (elements) of the row of (face, side) slot k = side * FT + lf
+template <typename R>
+__host__ __device__ constexpr int row_slot(int k) {
+    return FG4 ? (k >> 2) * g4_stride<R>() + (k & 3) * rstride<R>() : k * rstride<R>();
+}
+__host__ __device__ constexpr size_t align128(size_t x) { return (x + 127) & ~size_t(127); }
 template <typename T, typename R = double>
 __host__ __device__ constexpr size_t face_smem_bytes() {
-    return align16(16 + 4 * FBS * sizeof(T)) +
-           FNBUF * align16(cmax(size_t(2 * FT) * rstride<R>() * sizeof(R), size_t(2 * FT) * NQF * 5 * sizeof(T)));
+    return (FG4 ? align128(16 + 4 * FBS * sizeof(T)) : align16(16 + 4 * FBS * sizeof(T))) +
+           FNBUF * (FG4 ? align128(cmax(size_t(row_slot<R>(2 * FT)) * sizeof(R), size_t(2 * FT) * NQF * 5 * sizeof(T)))
+                        : align16(cmax(size_t(2 * FT) * rstride<R>() * sizeof(R),
+                                       size_t(2 * FT) * NQF * 5 * sizeof(T))));
 }
 
 // element kernel shared memory carve-up
@@ -383,19 +401,19 @@ __device__ __forceinline__ void face_moments(const T (&hq)[NQ], T (&fa)[N]) {
 //  kernel fetches a tile's records with one contiguous copy.
 template <typename T, bool BND, bool ES, typename R = double>
 __global__ void __launch_bounds__(FACE_THREADS, sizeof(T) == 4 ? HODG_FACE_MINB_F : HODG_FACE_MINB)
-    face_flux_kernel(const hodg_mesh_desc m,
-                                                                    const R* __restrict__ state,
-                                                                    T* __restrict__ hbuf,
-                                                                    uint32_t* __restrict__ err, int64_t f_begin,
-                                                                    int64_t f_end) {
+    face_flux_kernel(const hodg_mesh_desc m, const R* __restrict__ state, T* __restrict__ hbuf,
+                     uint32_t* __restrict__ err, int64_t f_begin, int64_t f_end,
+                     const __grid_constant__ CUtensorMap rmap) {
     constexpr int HS = hstride<T>();
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem);  // one per buffer
     T* fbt = reinterpret_cast<T*>(smem + 16);
     constexpr int RR = rstride<R>();
-    R* rows0 = reinterpret_cast<R*>(smem + align16(16 + 4 * FBS * sizeof(T)));
-    constexpr size_t BUF = align16(cmax(size_t(2 * FT) * RR * sizeof(R), size_t(2 * FT) * NQF * 5 * sizeof(T))) /
-                           sizeof(R);
+    R* rows0 = reinterpret_cast<R*>(smem + (FG4 ? align128(16 + 4 * FBS * sizeof(T)) : align16(16 + 4 * FBS * sizeof(T))));
+    constexpr size_t BUF =
+        (FG4 ? align128(cmax(size_t(row_slot<R>(2 * FT)) * sizeof(R), size_t(2 * FT) * NQF * 5 * sizeof(T)))
+             : align16(cmax(size_t(2 * FT) * RR * sizeof(R), size_t(2 * FT) * NQF * 5 * sizeof(T)))) /
+        sizeof(R);
     __shared__ double fn[2][FT][3];
     __shared__ int finf[2][FT];
     __shared__ int64_t fdst[2][FT][2];  // ES: record offsets of the left / right blocks (-1: none)
@@ -458,7 +476,20 @@ __global__ void __launch_bounds__(FACE_THREADS, sizeof(T) == 4 ? HODG_FACE_MINB_
             fn[buf][lf][1] = mt.nrm.y;
             fn[buf][lf][2] = mt.nrm.z;
         }
-        R* row = rows0 + buf * BUF + size_t(side * FT + lf) * RR;
+        R* row = rows0 + buf * BUF + row_slot<R>(side * FT + lf);
+        if constexpr (FG4) {
+            // faces lf .. lf+3 of this side sit NG lanes apart in the warp
+            const int e1 = __shfl_down_sync(0xffffffffu, mt.elem, NG);
+            const int e2 = __shfl_down_sync(0xffffffffu, mt.elem, 2 * NG);
+            const int e3 = __shfl_down_sync(0xffffffffu, mt.elem, 3 * NG);
+            if (g == 0 && (lf & 3) == 0) {
+                mbar_arrive_expect_tx(bar + buf, 4 * RR * sizeof(R));
+                tma_gather4(row, &rmap, mt.elem, e1, e2, e3, bar + buf);
+            } else {
+                mbar_arrive(bar + buf);
+            }
+            return;
+        }
 #if HODG_FACE_CPASYNC
         // the NG threads of this (face, side) copy the row in 16-byte
         // chunks, interleaved so each adjacent pair fills one 32-byte sector
@@ -501,7 +532,7 @@ __global__ void __launch_bounds__(FACE_THREADS, sizeof(T) == 4 ? HODG_FACE_MINB_
         mbar_wait(bar + buf, FNBUF == 2 ? ((it >> 1) & 1) : (it & 1));
 
         // phase 1: traces of this side at qps [g*QPT, g*QPT + QPT)
-        const R* myrow = rows0 + buf * BUF + size_t(side * FT + lf) * RR;
+        const R* myrow = rows0 + buf * BUF + row_slot<R>(side * FT + lf);
         T tr[QPT][5];
 #pragma unroll
         for (int qq = 0; qq < QPT; ++qq)
@@ -1296,8 +1327,10 @@ static int launch_face_k(const hodg_mesh_desc& m, const R* state, void* hbuf, ui
     if (launch_setup(lc, face_flux_kernel<T, BND, ES, R>, FACE_THREADS, sm, &cap) != HODG_OK) return HODG_ECUDA;
     const int64_t ntiles = (fe - fb + FT - 1) / FT;
     const int64_t nblk = ntiles < cap ? ntiles : cap;  // persistent CTAs loop over tiles
+    CUtensorMap rmap = {};
+    if (FG4 && nblk > 0 && encode_row_map(&rmap, state, rstride<R>(), int(sizeof(R))) != HODG_OK) return HODG_ECUDA;
     return launch_maybe_pdl(m, face_flux_kernel<T, BND, ES, R>, nblk, FACE_THREADS, sm, st, m, state,
-                            static_cast<T*>(hbuf), err, fb, fe);
+                            static_cast<T*>(hbuf), err, fb, fe, rmap);
 }
 
 // interior_only: every face in [fb, fe) has a right element (no boundary
