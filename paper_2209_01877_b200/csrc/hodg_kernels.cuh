@@ -288,13 +288,27 @@ constexpr bool EPERSIST = HODG_EPERSIST && !WARP_ELEM && ORDER <= 2 && H == 1;
 #define HODG_RED_HT 1
 #endif
 
+// face-ordered records by TMA tile::gather4 (four records per instruction)
+// where the packed layout is the one the gather reads anyway: records of
+// hsmem == hstride elements whose groups of four fill whole 128-byte lines
+// (FP64 P2: 36 doubles); elsewhere one bulk copy per record
+#ifndef HODG_ELEM_G4
+#define HODG_ELEM_G4 1
+#endif
+template <typename T>
+__host__ __device__ constexpr bool elem_g4() {
+    return HODG_ELEM_G4 && !HODG_ELEM_CPASYNC && hsmem<T>() == hstride<T>() &&
+           (4 * hstride<T>() * sizeof(T)) % 128 == 0;
+}
+
 template <typename T, bool ES>
 struct ElemSmem {
     static constexpr int NGB = EPERSIST ? 2 : 1;
     static constexpr size_t bar = 0;                                         // in[2], records, u0 tile
     static constexpr size_t geo = 32;                                        // NGB x 16 x E doubles (tiled)
     static constexpr size_t fid = geo + size_t(NGB) * 16 * E * 8;            // NGB x 4 x E int32 (tiled)
-    static constexpr size_t htile = align16(fid + size_t(NGB) * 4 * E * 4);  // state tile, then the records
+    static constexpr size_t htile = !ES && elem_g4<T>() ? align128(fid + size_t(NGB) * 4 * E * 4)
+                                                        : align16(fid + size_t(NGB) * 4 * E * 4);  // state tile, then the records
     static constexpr size_t hrec = ES ? size_t(E) * EREC * sizeof(T) : size_t(4) * E * hsmem<T>() * sizeof(T);
     static constexpr size_t sbytes = size_t(E) * RS * 8;
     static constexpr size_t hbytes = EPERSIST ? cmax(hrec, sbytes) : hrec;
@@ -676,11 +690,11 @@ __global__ void __launch_bounds__(FACE_THREADS, sizeof(T) == 4 ? HODG_FACE_MINB_
 template <typename T, bool ES>
 __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : HODG_EMINB_F) : EMINB)
     elem_stage_kernel(const hodg_mesh_desc m, const T* __restrict__ hbuf, const hodg_stage_args a,
-                      uint32_t* __restrict__ err) {
+                      uint32_t* __restrict__ err, const __grid_constant__ CUtensorMap hmap) {
     using L = ElemSmem<T, ES>;
     constexpr int HS = hstride<T>();
     constexpr int HSS = hsmem<T>();
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::bar);  // [0, 1] inputs per buffer, [2] records, [3] u0
     T* HT = reinterpret_cast<T*>(smem + L::htile);
     // the state tile: in the record region when persistent (the next tile's
@@ -797,8 +811,23 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : HODG_E
             }
             cp_async_arrive(bar + 2);
 #else
-            // thread (s, e) for t < 4E fetches face FI[s][e]
-            if (t < 4 * E) {
+            if constexpr (elem_g4<T>()) {
+                // thread (s, e), e % 4 == 0, gathers faces FI[s][e .. e+3]
+                // (rows past the tile's end: index -1, zero-filled)
+                if (t < 4 * E) {
+                    if ((t & 3) == 0) {
+                        const int4 f4 = *reinterpret_cast<const int4*>(FI + t);
+                        const int eb = t % E;
+                        fence_proxy_async();
+                        mbar_arrive_expect_tx(bar + 2, 4 * HS * sizeof(T));
+                        tma_gather4(HT + size_t(t) * HSS, &hmap, eb < ne ? f4.x : -1, eb + 1 < ne ? f4.y : -1,
+                                    eb + 2 < ne ? f4.z : -1, eb + 3 < ne ? f4.w : -1, bar + 2);
+                    } else {
+                        mbar_arrive(bar + 2);
+                    }
+                }
+            } else if (t < 4 * E) {
+                // thread (s, e) for t < 4E fetches face FI[s][e]
                 if (t % E < ne) {
                     fence_proxy_async();
                     mbar_arrive_expect_tx(bar + 2, HS * sizeof(T));
@@ -1374,8 +1403,11 @@ static int launch_elem_k(const hodg_mesh_desc& m, const void* hbuf, const hodg_s
         if (launch_setup(lc, elem_stage_kernel<T, ES>, ETHREADS, sm, &cap) != HODG_OK) return HODG_ECUDA;
         const int64_t ntiles = (m.n_elems + E - 1) / E;
         const int64_t nblk = EPERSIST && ntiles > cap ? cap : ntiles;  // persistent CTAs loop over tiles
+        CUtensorMap hmap = {};
+        if (!ES && elem_g4<T>() && nblk > 0 && encode_row_map(&hmap, hbuf, hstride<T>(), int(sizeof(T))) != HODG_OK)
+            return HODG_ECUDA;
         return launch_maybe_pdl(m, elem_stage_kernel<T, ES>, nblk, ETHREADS, sm, st, m, static_cast<const T*>(hbuf),
-                                a, err);
+                                a, err, hmap);
     }
 }
 
