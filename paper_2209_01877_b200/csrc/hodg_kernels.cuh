@@ -288,17 +288,22 @@ constexpr bool EPERSIST = HODG_EPERSIST && !WARP_ELEM && ORDER <= 2 && H == 1;
 #define HODG_RED_HT 1
 #endif
 
-// face-ordered records by TMA tile::gather4 (four records per instruction)
-// where the packed layout is the one the gather reads anyway: records of
-// hsmem == hstride elements whose groups of four fill whole 128-byte lines
-// (FP64 P2: 36 doubles); elsewhere one bulk copy per record
+// face-ordered records by TMA tile::gather4 (four records per instruction),
+// in 128-byte-aligned groups of four.  1: FP64 (P0 / P1 / P2 element kernel
+// 0.128 / 0.252 / 0.464 -> 0.109 / 0.240 / 0.444 ms at C1M); 2: also FP32,
+// whose groups put a warp's record reads on few banks (P2 0.345 -> 0.388 ms)
 #ifndef HODG_ELEM_G4
 #define HODG_ELEM_G4 1
 #endif
 template <typename T>
 __host__ __device__ constexpr bool elem_g4() {
-    return HODG_ELEM_G4 && !HODG_ELEM_CPASYNC && hsmem<T>() == hstride<T>() &&
-           (4 * hstride<T>() * sizeof(T)) % 128 == 0;
+    return !HODG_ELEM_CPASYNC && (HODG_ELEM_G4 == 2 || (HODG_ELEM_G4 == 1 && sizeof(T) == 8));
+}
+// smem offset (elements) of face record r = s * E + e in the face-ordered tile
+template <typename T>
+__host__ __device__ constexpr int rec_slot(int r) {
+    return elem_g4<T>() ? (r >> 2) * int(align128(4 * hstride<T>() * sizeof(T)) / sizeof(T)) + (r & 3) * hstride<T>()
+                        : r * hsmem<T>();
 }
 
 template <typename T, bool ES>
@@ -309,7 +314,7 @@ struct ElemSmem {
     static constexpr size_t fid = geo + size_t(NGB) * 16 * E * 8;            // NGB x 4 x E int32 (tiled)
     static constexpr size_t htile = !ES && elem_g4<T>() ? align128(fid + size_t(NGB) * 4 * E * 4)
                                                         : align16(fid + size_t(NGB) * 4 * E * 4);  // state tile, then the records
-    static constexpr size_t hrec = ES ? size_t(E) * EREC * sizeof(T) : size_t(4) * E * hsmem<T>() * sizeof(T);
+    static constexpr size_t hrec = ES ? size_t(E) * EREC * sizeof(T) : size_t(rec_slot<T>(4 * E)) * sizeof(T);
     static constexpr size_t sbytes = size_t(E) * RS * 8;
     static constexpr size_t hbytes = EPERSIST ? cmax(hrec, sbytes) : hrec;
     static constexpr size_t sx = align16(htile + hbytes);
@@ -820,7 +825,7 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : HODG_E
                         const int eb = t % E;
                         fence_proxy_async();
                         mbar_arrive_expect_tx(bar + 2, 4 * HS * sizeof(T));
-                        tma_gather4(HT + size_t(t) * HSS, &hmap, eb < ne ? f4.x : -1, eb + 1 < ne ? f4.y : -1,
+                        tma_gather4(HT + rec_slot<T>(t), &hmap, eb < ne ? f4.x : -1, eb + 1 < ne ? f4.y : -1,
                                     eb + 2 < ne ? f4.z : -1, eb + 3 < ne ? f4.w : -1, bar + 2);
                     } else {
                         mbar_arrive(bar + 2);
@@ -1000,7 +1005,7 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : HODG_E
             hsel(h, [&](auto hc) {
                 sfor<4>([&](auto s) {
                     const T* hrec =
-                        ES ? HT + size_t(e) * EREC + s * HSE + v * NQF : HT + size_t(s * E + e) * HSS + v * NQF;
+                        ES ? HT + size_t(e) * EREC + s * HSE + v * NQF : HT + rec_slot<T>(s * E + e) + v * NQF;
                     T hq[NQF];
                     if constexpr (ES) {
 #pragma unroll
