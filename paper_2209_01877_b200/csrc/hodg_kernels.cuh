@@ -58,8 +58,16 @@ constexpr int FACE_THREADS = 128;
 #ifndef HODG_FACE_MINB
 #define HODG_FACE_MINB (ORDER == 2 ? 4 : 5)
 #endif
+// CTA element kernel, face-ordered records: 16-byte cp.async chunks (1) or
+// TMA copies (0: gather4 / one per record).  FP64: TMA gather4 is faster;
+// FP32: cp.async (P2 element kernel 0.346 -> 0.335 ms, P1 0.201 -> 0.192 ms
+// at C1M) -- its records' padded stride keeps the reads conflict-free,
+// which gather4's 128-byte groups would not
 #ifndef HODG_ELEM_CPASYNC
-#define HODG_ELEM_CPASYNC 0  // CTA element kernel: face records by cp.async chunks (0: one TMA copy per record; faster)
+#define HODG_ELEM_CPASYNC 0
+#endif
+#ifndef HODG_ELEM_CPASYNC_F
+#define HODG_ELEM_CPASYNC_F 1
 #endif
 #ifndef HODG_FACE_CPASYNC
 #define HODG_FACE_CPASYNC 0  // state rows by per-thread cp.async chunks (0: one TMA bulk copy per row; faster)
@@ -297,7 +305,8 @@ constexpr bool EPERSIST = HODG_EPERSIST && !WARP_ELEM && ORDER <= 2 && H == 1;
 #endif
 template <typename T>
 __host__ __device__ constexpr bool elem_g4() {
-    return !HODG_ELEM_CPASYNC && (HODG_ELEM_G4 == 2 || (HODG_ELEM_G4 == 1 && sizeof(T) == 8));
+    return !(sizeof(T) == 4 ? HODG_ELEM_CPASYNC_F : HODG_ELEM_CPASYNC) &&
+           (HODG_ELEM_G4 == 2 || (HODG_ELEM_G4 == 1 && sizeof(T) == 8));
 }
 // smem offset (elements) of face record r = s * E + e in the face-ordered tile
 template <typename T>
@@ -699,6 +708,7 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : HODG_E
     using L = ElemSmem<T, ES>;
     constexpr int HS = hstride<T>();
     constexpr int HSS = hsmem<T>();
+    constexpr bool ECPA = sizeof(T) == 4 ? HODG_ELEM_CPASYNC_F : HODG_ELEM_CPASYNC;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::bar);  // [0, 1] inputs per buffer, [2] records, [3] u0
     T* HT = reinterpret_cast<T*>(smem + L::htile);
@@ -737,7 +747,7 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : HODG_E
         if (a.dt_reset && blockIdx.x == 0) *a.dt_reset = 0x7FF0000000000000ull;
         mbar_init(bar, 1);
         mbar_init(bar + 1, 1);
-        mbar_init(bar + 2, ES ? 1 : (HODG_ELEM_CPASYNC ? ETHREADS : 4 * E));
+        mbar_init(bar + 2, ES ? 1 : (ECPA ? ETHREADS : 4 * E));
         mbar_init(bar + 3, 1);
         mbar_fence_init();
         if (tile < ntiles) issue_inputs(tile, 0);  // the stage state: two launches back
@@ -802,8 +812,7 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : HODG_E
             } else if (t == 0) {
                 mbar_arrive(bar + 2);
             }
-        } else {
-#if HODG_ELEM_CPASYNC
+        } else if constexpr (ECPA) {
             // 16-byte cp.async chunks, consecutive threads on consecutive
             // chunks of one record; every thread arrives once when its copies land
             constexpr int NC = int(HS * sizeof(T) / 16);
@@ -815,7 +824,7 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : HODG_E
                                reinterpret_cast<const char*>(hbuf + int64_t(FI[r]) * HS) + 16 * k);
             }
             cp_async_arrive(bar + 2);
-#else
+        } else {
             if constexpr (elem_g4<T>()) {
                 // thread (s, e), e % 4 == 0, gathers faces FI[s][e .. e+3]
                 // (rows past the tile's end: index -1, zero-filled)
@@ -841,7 +850,6 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : HODG_E
                     mbar_arrive(bar + 2);
                 }
             }
-#endif
         }
 
         T acc[NH];
