@@ -263,6 +263,15 @@ constexpr int FNBUF = HODG_FACE_NBUF;
 #define HODG_FACE_G4 1
 #endif
 constexpr bool FG4 = HODG_FACE_G4 && !HODG_FACE_CPASYNC;
+// phase-1 traces without per-qp branches or zero-initialised accumulators
+// (1: except FP64 P3, where it measured 0.704 -> 0.750 ms; 2: everywhere)
+#ifndef HODG_FACE_P1_FLAT
+#define HODG_FACE_P1_FLAT 1
+#endif
+template <typename T>
+__host__ __device__ constexpr bool face_p1_flat() {
+    return HODG_FACE_P1_FLAT == 2 || (HODG_FACE_P1_FLAT == 1 && !(ORDER == 3 && sizeof(T) == 8));
+}
 template <typename R>
 __host__ __device__ constexpr int g4_stride() {  // elements per group of four rows
     return int((4 * rstride<R>() * sizeof(R) + 127) / 128 * 128 / sizeof(R));
@@ -562,13 +571,39 @@ __global__ void __launch_bounds__(FACE_THREADS, sizeof(T) == 4 ? HODG_FACE_MINB_
         // phase 1: traces of this side at qps [g*QPT, g*QPT + QPT)
         const R* myrow = rows0 + buf * BUF + row_slot<R>(side * FT + lf);
         T tr[QPT][5];
+        if constexpr (!face_p1_flat<T>()) {
 #pragma unroll
-        for (int qq = 0; qq < QPT; ++qq)
+            for (int qq = 0; qq < QPT; ++qq)
 #pragma unroll
-            for (int v = 0; v < 5; ++v) tr[qq][v] = T(0);
-        if (cur.elem >= 0) {
+                for (int v = 0; v < 5; ++v) tr[qq][v] = T(0);
+            if (cur.elem >= 0) {
+                const int slot = side == 0 ? (cur.info & 3) : ((cur.info >> 2) & 3);
+                const T* fb = fbt + slot * FBS;
+#pragma unroll
+                for (int i = 0; i < NB; ++i) {
+                    T c[5];
+#pragma unroll
+                    for (int v = 0; v < 5; ++v) c[v] = T(myrow[v * NB + i]);
+#pragma unroll
+                    for (int qq = 0; qq < QPT; ++qq) {
+                        const int q = g * QPT + qq;
+                        if (NG * QPT == NQF || q < NQF) {
+                            const T b = fb[q * NB + i];
+#pragma unroll
+                            for (int v = 0; v < 5; ++v) tr[qq][v] += b * c[v];
+                        }
+                    }
+                }
+            }
+        } else if (FG4 || cur.elem >= 0) {
+            // (gather4 zero-fills the rows of absent elements: no branch)
             const int slot = side == 0 ? (cur.info & 3) : ((cur.info >> 2) & 3);
             const T* fb = fbt + slot * FBS;
+            // a group's qps past NQF repeat the last one (not stored): no
+            // per-qp branch inside the basis loop
+            int qo[QPT];
+#pragma unroll
+            for (int qq = 0; qq < QPT; ++qq) qo[qq] = min(g * QPT + qq, NQF - 1) * NB;
 #pragma unroll
             for (int i = 0; i < NB; ++i) {
                 T c[5];
@@ -576,14 +611,16 @@ __global__ void __launch_bounds__(FACE_THREADS, sizeof(T) == 4 ? HODG_FACE_MINB_
                 for (int v = 0; v < 5; ++v) c[v] = T(myrow[v * NB + i]);
 #pragma unroll
                 for (int qq = 0; qq < QPT; ++qq) {
-                    const int q = g * QPT + qq;
-                    if (NG * QPT == NQF || q < NQF) {
-                        const T b = fb[q * NB + i];
+                    const T b = fb[qo[qq] + i];
 #pragma unroll
-                        for (int v = 0; v < 5; ++v) tr[qq][v] += b * c[v];
-                    }
+                    for (int v = 0; v < 5; ++v) tr[qq][v] = i == 0 ? b * c[v] : tr[qq][v] + b * c[v];
                 }
             }
+        } else {
+#pragma unroll
+            for (int qq = 0; qq < QPT; ++qq)
+#pragma unroll
+                for (int v = 0; v < 5; ++v) tr[qq][v] = T(0);
         }
         __syncthreads();  // rows[buf] consumed; previous tile's phase 2 done everywhere
         T* trs = reinterpret_cast<T*>(rows0 + buf * BUF);
