@@ -735,6 +735,13 @@ __global__ void __launch_bounds__(FACE_THREADS, sizeof(T) == 4 ? HODG_FACE_MINB_
 // the hot phases is unit-stride across the warp.
 // ES: the records are in the element-slot layout -- one bulk copy of the
 // tile's record blocks, issued with the state tile, no per-face gather.
+#ifndef HODG_MP_FACE_F32
+// mixed: face terms of the element residual accumulated in FP32 (as the
+// volume term), one conversion for the FP64 solve -- P1 / P3 element kernel
+// 0.192 / 0.552 -> 0.181 / 0.534 ms; at P2 the FP64 accumulation measured
+// faster (0.335 vs 0.340 ms)
+#define HODG_MP_FACE_F32 (ORDER != 2)
+#endif
 #ifndef HODG_EMINB_F
 #define HODG_EMINB_F 6  // mixed-precision element kernel at P0-P2 (64 registers; RED / FP32 tile in the record region)
 #endif
@@ -1045,6 +1052,9 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : HODG_E
         mbar_wait(bar + 2, it & 1);
         double accd[NH];
         if (live) {
+            // FP64: the face terms accumulate in FP64; mixed: in FP32, as the
+            // volume term (the reference's float32 rhs_pass), converted once
+            // for the FP64 mass solve
 #pragma unroll
             for (int i = 0; i < NH; ++i) accd[i] = double(acc[i]);
             hsel(h, [&](auto hc) {
@@ -1066,10 +1076,20 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : HODG_E
                     T fa[NH];
                     face_moments<T, s, hc * NH, NH>(hq, fa);
                     const double fc = G[(9 + s) * E + e];
+                    if constexpr (sizeof(T) == 8 || !HODG_MP_FACE_F32) {
 #pragma unroll
-                    for (int i = 0; i < NH; ++i) accd[i] -= fc * double(fa[i]);
+                        for (int i = 0; i < NH; ++i) accd[i] -= fc * double(fa[i]);
+                    } else {
+                        const T fcf = T(fc);
+#pragma unroll
+                        for (int i = 0; i < NH; ++i) acc[i] -= fcf * fa[i];
+                    }
                 });
             });
+            if constexpr (sizeof(T) == 4 && HODG_MP_FACE_F32) {
+#pragma unroll
+                for (int i = 0; i < NH; ++i) accd[i] = double(acc[i]);
+            }
         }
         double full[H == 1 ? 1 : NB];
         if constexpr (H > 1) {
