@@ -112,6 +112,11 @@ static inline int encode_row_map(CUtensorMap* tm, const void* base, int cols, in
     return r == CUDA_SUCCESS ? HODG_OK : HODG_ECUDA;
 }
 
+// global -> L2 prefetch of a contiguous range (no completion tracking)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // shared -> global (bulk group); caller waits with bulk_wait_read()
 __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),

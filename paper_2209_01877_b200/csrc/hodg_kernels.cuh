@@ -735,6 +735,11 @@ __global__ void __launch_bounds__(FACE_THREADS, sizeof(T) == 4 ? HODG_FACE_MINB_
 // the hot phases is unit-stride across the warp.
 // ES: the records are in the element-slot layout -- one bulk copy of the
 // tile's record blocks, issued with the state tile, no per-face gather.
+// element kernel: L2 prefetch distance in tiles (0: off)
+#ifndef HODG_EPF_DIST
+#define HODG_EPF_DIST 0
+#endif
+constexpr int EPF_DIST = HODG_EPF_DIST;
 #ifndef HODG_MP_FACE_F32
 // mixed: face terms of the element residual accumulated in FP32 (as the
 // volume term), one conversion for the FP64 solve -- P1 / P3 element kernel
@@ -795,6 +800,17 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : HODG_E
         mbar_init(bar + 3, 1);
         mbar_fence_init();
         if (tile < ntiles) issue_inputs(tile, 0);  // the stage state: two launches back
+        if constexpr (EPF_DIST > 0) {
+            // warm L2 with the inputs of the tile a CTA will start about one
+            // wave later, so its first TMA wait is an L2 round trip
+            const int64_t pt = tile + EPF_DIST;
+            if (!EPERSIST && pt < ntiles) {
+                const int nn = int(min(int64_t(E), m.n_elems - pt * E));
+                bulk_prefetch_l2(a.us + pt * E * RS, uint32_t(nn) * RS * 8);
+                bulk_prefetch_l2(m.egeo + pt * 16 * E, 16 * E * 8);
+                if (need_u0 && a.u0 != a.us) bulk_prefetch_l2(a.u0 + pt * E * RS, uint32_t(nn) * RS * 8);
+            }
+        }
     }
     // programmatic dependent launch: everything above overlapped the face
     // kernel's tail; records, and the in-place output, need it complete
@@ -857,15 +873,24 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : HODG_E
                 mbar_arrive(bar + 2);
             }
         } else if constexpr (ECPA) {
-            // 16-byte cp.async chunks, consecutive threads on consecutive
-            // chunks of one record; every thread arrives once when its copies land
+            // 16-byte cp.async chunks: thread (row rr, chunk k) of RPR rows
+            // per round copies chunk k of records rr, rr + RPR, ... (the
+            // division is done once); every thread arrives once when its
+            // copies land
             constexpr int NC = int(HS * sizeof(T) / 16);
-            for (int cc = t; cc < 4 * E * NC; cc += ETHREADS) {
-                const int r = cc / NC;
-                const int k = cc - r * NC;
-                if (r % E < ne)
-                    cp_async16(reinterpret_cast<char*>(HT + size_t(r) * HSS) + 16 * k,
-                               reinterpret_cast<const char*>(hbuf + int64_t(FI[r]) * HS) + 16 * k);
+            constexpr int RPR = ETHREADS / NC;
+            constexpr int NR = (4 * E + RPR - 1) / RPR;
+            if (t < RPR * NC) {
+                const int rr = t / NC;
+                const int k = t - rr * NC;
+                const char* src = reinterpret_cast<const char*>(hbuf) + 16 * k;
+                char* dst = reinterpret_cast<char*>(HT) + 16 * k;
+#pragma unroll
+                for (int j = 0; j < NR; ++j) {
+                    const int r = rr + j * RPR;
+                    if ((NR * RPR == 4 * E || r < 4 * E) && r % E < ne)
+                        cp_async16(dst + size_t(r) * HSS * sizeof(T), src + int64_t(FI[r]) * (HS * sizeof(T)));
+                }
             }
             cp_async_arrive(bar + 2);
         } else {
