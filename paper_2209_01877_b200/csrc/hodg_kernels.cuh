@@ -48,7 +48,10 @@ __host__ __device__ constexpr int rstride() {
 // face qp groups per side thread (phase 1): bounds the trace accumulators
 constexpr int NG = ORDER == 3 ? HODG_NG3 : (ORDER == 2 ? HODG_NG2 : (ORDER == 1 ? HODG_NG1 : 1));
 constexpr int QPT = (NQF + NG - 1) / NG;     // face qps per phase-1 thread
-constexpr int FACE_THREADS = 128;
+#ifndef HODG_FACE_THREADS
+#define HODG_FACE_THREADS 128
+#endif
+constexpr int FACE_THREADS = HODG_FACE_THREADS;
 #ifndef HODG_ROE_PAIRS
 #define HODG_ROE_PAIRS 1
 #endif
@@ -437,7 +440,7 @@ __device__ __forceinline__ void face_moments(const T (&hq)[NQ], T (&fa)[N]) {
 //  record is stored in the blocks of both (owned) neighbours, so the element
 //  kernel fetches a tile's records with one contiguous copy.
 template <typename T, bool BND, bool ES, typename R = double>
-__global__ void __launch_bounds__(FACE_THREADS, sizeof(T) == 4 ? HODG_FACE_MINB_F : HODG_FACE_MINB)
+__global__ void __launch_bounds__(FACE_THREADS, (sizeof(T) == 4 ? HODG_FACE_MINB_F : HODG_FACE_MINB) * 128 / FACE_THREADS)
     face_flux_kernel(const hodg_mesh_desc m, const R* __restrict__ state, T* __restrict__ hbuf,
                      uint32_t* __restrict__ err, int64_t f_begin, int64_t f_end,
                      const __grid_constant__ CUtensorMap rmap) {
