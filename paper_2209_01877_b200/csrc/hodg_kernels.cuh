@@ -746,9 +746,10 @@ constexpr int EPF_DIST = HODG_EPF_DIST;
 #ifndef HODG_MP_FACE_F32
 // mixed: face terms of the element residual accumulated in FP32 (as the
 // volume term), one conversion for the FP64 solve -- P1 / P3 element kernel
-// 0.192 / 0.552 -> 0.181 / 0.534 ms; at P2 the FP64 accumulation measured
-// faster (0.335 vs 0.340 ms)
-#define HODG_MP_FACE_F32 (ORDER != 2)
+// 0.192 / 0.552 -> 0.181 / 0.534 ms, P2 0.335 -> 0.340 ms.  Off: the
+// reference's float32 rhs_pass adds each face term into its FP64 scratch
+// (SURVEY.md appendix A), which the default keeps
+#define HODG_MP_FACE_F32 0
 #endif
 #ifndef HODG_EMINB_F
 #define HODG_EMINB_F 6  // mixed-precision element kernel at P0-P2 (64 registers; RED / FP32 tile in the record region)
@@ -1080,9 +1081,9 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : HODG_E
         mbar_wait(bar + 2, it & 1);
         double accd[NH];
         if (live) {
-            // FP64: the face terms accumulate in FP64; mixed: in FP32, as the
-            // volume term (the reference's float32 rhs_pass), converted once
-            // for the FP64 mass solve
+            // the four face terms are added in FP64 (the reference's float32
+            // rhs_pass adds its FP32 products into an FP64 scratch);
+            // HODG_MP_FACE_F32 sums them in FP32 first
 #pragma unroll
             for (int i = 0; i < NH; ++i) accd[i] = double(acc[i]);
             hsel(h, [&](auto hc) {
