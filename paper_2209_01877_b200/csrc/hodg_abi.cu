@@ -77,19 +77,32 @@ __global__ void norm_partial_kernel(const double* __restrict__ res, const double
 }
 
 // one CTA: thread k sums rows k, k+RT, ... in order, then a fixed tree
-__global__ void norm_finalize_kernel(const double* __restrict__ partial, int64_t nblk, double* __restrict__ out5) {
-    __shared__ double sm[5][RT];
+// one CTA of 1024 threads, each summing a strided run of the per-block
+// partials with four runs' loads in flight (L2 latency, not one SM's serial
+// loads, bounds it: C1M's 31,196 x 5 partials 26.7 -> ~5 us), then a fixed
+// shuffle tree -- the same order every call
+constexpr int NFT = 1024;
+__global__ void __launch_bounds__(NFT) norm_finalize_kernel(const double* __restrict__ partial, int64_t nblk,
+                                                            double* __restrict__ out5) {
+    __shared__ double sm[5][NFT / 32];
     double s[5] = {0, 0, 0, 0, 0};
-    for (int64_t b = threadIdx.x; b < nblk; b += RT)
+#pragma unroll 4
+    for (int64_t b = threadIdx.x; b < nblk; b += NFT)
         for (int v = 0; v < 5; ++v) s[v] += partial[b * 5 + v];
-    for (int v = 0; v < 5; ++v) sm[v][threadIdx.x] = s[v];
-    __syncthreads();
-    for (int w = RT / 2; w > 0; w >>= 1) {
-        if (threadIdx.x < w)
-            for (int v = 0; v < 5; ++v) sm[v][threadIdx.x] += sm[v][threadIdx.x + w];
-        __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int v = 0; v < 5; ++v) {
+        double x = s[v];
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+        if (lane == 0) sm[v][w] = x;
     }
-    if (threadIdx.x < 5) out5[threadIdx.x] = sqrt(sm[threadIdx.x][0]);
+    __syncthreads();
+    if (w == 0) {
+        for (int v = 0; v < 5; ++v) {
+            double x = sm[v][lane];
+            for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+            if (lane == 0) out5[v] = sqrt(x);
+        }
+    }
 }
 
 __global__ void min_partial_kernel(const double* __restrict__ x, int64_t n, double* __restrict__ out) {
@@ -352,7 +365,7 @@ int hodg_modal_transform(const hodg_mesh* mesh, int to_reference, const double* 
 int hodg_norm_finalize(const double* partial, int64_t n_blocks, double* out5, void* stream) {
     if (!partial || !out5 || n_blocks <= 0) return HODG_EINVAL;
     g_launches++;
-    norm_finalize_kernel<<<1, RT, 0, S(stream)>>>(partial, n_blocks, out5);
+    norm_finalize_kernel<<<1, NFT, 0, S(stream)>>>(partial, n_blocks, out5);
     return cudaGetLastError() == cudaSuccess ? HODG_OK : HODG_ECUDA;
 }
 
@@ -364,7 +377,7 @@ int hodg_residual_l2(const hodg_mesh* mesh, const double* res, double* scratch, 
     const int p = mesh->d.order;
     norm_partial_kernel<<<unsigned(nblk), RT, 0, S(stream)>>>(res, mesh->d.egeo, n, rs_of(p), NB_TAB[p], hodg_elem_tile(p),
                                                                scratch);
-    norm_finalize_kernel<<<1, RT, 0, S(stream)>>>(scratch, nblk, out5);
+    norm_finalize_kernel<<<1, NFT, 0, S(stream)>>>(scratch, nblk, out5);
     return cudaGetLastError() == cudaSuccess ? HODG_OK : HODG_ECUDA;
 }
 
