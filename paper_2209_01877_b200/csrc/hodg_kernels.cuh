@@ -819,6 +819,7 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : HODG_E
     const int v = t / (E * H);
     const int jb = h * NH;  // first basis function of this thread's part
     const bool need_u0 = a.combine == 1 || (a.combine == 0 && a.a != 0.0);
+    const bool need_mean = a.combine >= 0 && (a.dt_next || a.dt_vec_out);
     const T gam = T(m.gamma);
 
     auto issue_inputs = [&](int64_t tl, int gb) {  // thread 0
@@ -1219,7 +1220,7 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : HODG_E
                             if (a.a != 0.0) o = a.a * u0j + o;
                         }
                         outr[j] = o;
-                        mean += MEAN_T[hc * NH + j] * o;
+                        if (need_mean) mean += MEAN_T[hc * NH + j] * o;  // (the dt epilogue's cell mean)
                     });
                 });
                 if constexpr (H == 1 && (NB % 2) == 0) {
@@ -1236,7 +1237,7 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : HODG_E
                         for (int j = 0; j < NH; ++j) S32[e * RSF + v * NB + jb + j] = float(outr[j]);
                     }
                 }
-                RED[5 * E + h * 5 * E + v * E + e] = mean;
+                if (need_mean) RED[5 * E + h * 5 * E + v * E + e] = mean;
             }
         }
         fence_proxy_async();
