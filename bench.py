@@ -318,8 +318,17 @@ def run_ours(args):
     # ---- end to end through the public stepping API ----
     host = state_in.coeffs.cpu().pin_memory()
     out_host = torch.empty_like(host).pin_memory()
-    norms = torch.empty(5, dtype=torch.float64).pin_memory()
-    errh = torch.empty(4, dtype=torch.int32).pin_memory()
+    # per-step reads into a two-slot pinned ring: step k's norms / error word
+    # are copied right after its launch and checked on the host while step
+    # k + 1 runs (every step is read and checked; the GPU never waits on it)
+    norms = [torch.empty(5, dtype=torch.float64).pin_memory() for _ in range(2)]
+    errh = [torch.empty(4, dtype=torch.int32).pin_memory() for _ in range(2)]
+    done = [torch.cuda.Event() for _ in range(2)]
+
+    def read_ok(k):
+        done[k % 2].synchronize()
+        return not (np.any(errh[k % 2].numpy().astype(np.uint32) != 0xFFFFFFFF)
+                    or not np.all(np.isfinite(norms[k % 2].numpy())))
 
     def e2e_pass():
         barrier()
@@ -327,14 +336,16 @@ def run_ours(args):
         t0 = time.perf_counter()
         dev_state = P.DofState(host.to("cuda", non_blocking=True))
         st.load(dev_state)
-        for _ in range(args.steps):
+        for k in range(args.steps):
             # (distributed: every rank reads its norms / error word each step)
             st.step()
-            norms.copy_(st.norms, non_blocking=True)
-            errh.copy_(disc.err, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
-            if np.any(errh.numpy().astype(np.uint32) != 0xFFFFFFFF) or not np.all(np.isfinite(norms.numpy())):
-                raise RuntimeError("solver error during e2e run")
+            norms[k % 2].copy_(st.norms, non_blocking=True)
+            errh[k % 2].copy_(disc.err, non_blocking=True)
+            done[k % 2].record()
+            if k > 0 and not read_ok(k - 1):
+                raise RuntimeError(f"solver error during e2e run (step {k - 1})")
+        if not read_ok(args.steps - 1):
+            raise RuntimeError("solver error during e2e run (last step)")
         out_host.copy_(st.state().coeffs, non_blocking=True)
         torch.cuda.synchronize()
         return time.perf_counter() - t0
