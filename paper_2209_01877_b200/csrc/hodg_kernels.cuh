@@ -56,7 +56,10 @@ constexpr int FACE_THREADS = HODG_FACE_THREADS;
 #define HODG_ROE_PAIRS 1
 #endif
 #ifndef HODG_FACE_MINB_F
-#define HODG_FACE_MINB_F 6  // mixed-precision face kernel: CTAs per SM of the register budget (80 registers)
+// mixed-precision face kernel: CTAs per SM of the register budget (6: 80
+// registers; P2 with the FFMA2 trace pairs: 5 at 96 registers, no spills --
+// face 0.326 -> 0.294 ms, where 6 spills 40 bytes)
+#define HODG_FACE_MINB_F (ORDER == 2 ? 5 : 6)
 #endif
 #ifndef HODG_FACE_MINB
 #define HODG_FACE_MINB (ORDER == 2 ? 4 : 5)
@@ -270,6 +273,10 @@ constexpr bool FG4 = HODG_FACE_G4 && !HODG_FACE_CPASYNC;
 // (1: except FP64 P3, where it measured 0.704 -> 0.750 ms; 2: everywhere)
 #ifndef HODG_FACE_P1_FLAT
 #define HODG_FACE_P1_FLAT 1
+#endif
+// FP32 contractions as packed f32x2 FMAs (FFMA2: two FMAs per issue slot)
+#ifndef HODG_FFMA2
+#define HODG_FFMA2 1
 #endif
 // phase-1 coefficient loads in pairs (one 16-byte / 8-byte shared load):
 // measured off -- FP64 P2 face 0.462 vs 0.463 ms, mixed 0.297 -> 0.304 ms
@@ -612,7 +619,40 @@ __global__ void __launch_bounds__(FACE_THREADS, (sizeof(T) == 4 ? HODG_FACE_MINB
             int qo[QPT];
 #pragma unroll
             for (int qq = 0; qq < QPT; ++qq) qo[qq] = min(g * QPT + qq, NQF - 1) * NB;
-            if constexpr (HODG_FACE_VEC && NB % 2 == 0) {
+            if constexpr (sizeof(T) == 4 && HODG_FFMA2 && QPT >= 2) {
+                // FP32: two qps per packed FFMA2 (sm_100 f32x2: the pair of
+                // table values against the coefficient broadcast) -- per
+                // lane the same FMUL / FFMA as the scalar loop
+                constexpr int NP = QPT / 2;
+                float2 t2[NP][5];
+#pragma unroll
+                for (int i = 0; i < NB; ++i) {
+                    float c[5];
+#pragma unroll
+                    for (int v = 0; v < 5; ++v) c[v] = float(myrow[v * NB + i]);
+#pragma unroll
+                    for (int pp = 0; pp < NP; ++pp) {
+                        const float2 b2 = make_float2(float(fb[qo[2 * pp] + i]), float(fb[qo[2 * pp + 1] + i]));
+#pragma unroll
+                        for (int v = 0; v < 5; ++v)
+                            t2[pp][v] = i == 0 ? __fmul2_rn(b2, make_float2(c[v], c[v]))
+                                               : __ffma2_rn(b2, make_float2(c[v], c[v]), t2[pp][v]);
+                    }
+                    if constexpr (QPT % 2 == 1) {
+                        const float b = float(fb[qo[QPT - 1] + i]);
+#pragma unroll
+                        for (int v = 0; v < 5; ++v)
+                            tr[QPT - 1][v] = i == 0 ? T(b * c[v]) : T(fmaf(b, c[v], float(tr[QPT - 1][v])));
+                    }
+                }
+#pragma unroll
+                for (int pp = 0; pp < NP; ++pp)
+#pragma unroll
+                    for (int v = 0; v < 5; ++v) {
+                        tr[2 * pp][v] = T(t2[pp][v].x);
+                        tr[2 * pp + 1][v] = T(t2[pp][v].y);
+                    }
+            } else if constexpr (HODG_FACE_VEC && NB % 2 == 0) {
                 // coefficient pairs (i, i+1) by one 16-byte (FP32: 8-byte)
                 // shared load; the sums keep the basis order
 #pragma unroll
@@ -1046,8 +1086,16 @@ __global__ void __launch_bounds__(ETHREADS, sizeof(T) == 4 ? (H > 1 ? 2 : HODG_E
                         const T fx = sl[v], fy = sl[5 + v], fz = sl[10 + v];
                         sfor<NBL>([&](auto j) {
                             const T wm = TAB(WV, T, (q0 + qq) * NB + j);
-                            mom[j][0] += wm * fx;
-                            mom[j][1] += wm * fy;
+                            if constexpr (sizeof(T) == 4 && HODG_FFMA2) {
+                                // (x, y) as one FFMA2 with the weight broadcast
+                                const float2 m2 = __ffma2_rn(make_float2(fx, fy), make_float2(wm, wm),
+                                                             make_float2(mom[j][0], mom[j][1]));
+                                mom[j][0] = m2.x;
+                                mom[j][1] = m2.y;
+                            } else {
+                                mom[j][0] += wm * fx;
+                                mom[j][1] += wm * fy;
+                            }
                             mom[j][2] += wm * fz;
                         });
                     });
