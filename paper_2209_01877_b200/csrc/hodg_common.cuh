@@ -283,6 +283,81 @@ __device__ __forceinline__ bool roe(const T qL[5], const T qR[5], const T n[3], 
     return ok;
 }
 
+// FP32 Roe-HH with the left / right states in packed f32x2 lanes (sm_100
+// FFMA2 / FMUL2 / FADD2: two operations per issue slot).  Same formulas as
+// roe<float>; the one-sided quantities (sqrt rho, 1/rho, velocities, p, H,
+// normal velocity) and the paired terms of the dissipation and the flux are
+// evaluated two at a time.
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ float2 f2b(float a) { return make_float2(a, a); }
+__device__ __forceinline__ bool roe_x2(const float qL[5], const float qR[5], const float n[3], float g, float f[5]) {
+    const float2 q0 = f2(qL[0], qR[0]), q1 = f2(qL[1], qR[1]), q2 = f2(qL[2], qR[2]), q3 = f2(qL[3], qR[3]),
+                 q4 = f2(qL[4], qR[4]);
+    const float2 is = f2(rsqrtf(qL[0]), rsqrtf(qR[0]));
+    const float2 ri = __fmul2_rn(is, is);
+    const float2 sq = __fmul2_rn(q0, is);  // sqrt(rho)
+    const float2 u = __fmul2_rn(q1, ri), v = __fmul2_rn(q2, ri), w = __fmul2_rn(q3, ri);
+    const float gm1 = g - 1.0f;
+    const float2 k2 = __ffma2_rn(w, w, __ffma2_rn(v, v, __fmul2_rn(u, u)));      // |u|^2
+    const float2 p = __fmul2_rn(f2b(gm1), __ffma2_rn(__fmul2_rn(f2b(-0.5f), q0), k2, q4));
+    const float nx = n[0], ny = n[1], nz = n[2];
+    const float2 vn = __ffma2_rn(w, f2b(nz), __ffma2_rn(v, f2b(ny), __fmul2_rn(u, f2b(nx))));
+    const float2 hh = __fmul2_rn(__fadd2_rn(q4, p), ri);                         // total enthalpy
+    const float di = rcp_nr(sq.x + sq.y);
+    // Roe averages: (sL xL + sR xR) / (sL + sR), two quantities per pair
+    const float2 su = __fmul2_rn(sq, u), sv = __fmul2_rn(sq, v), sw_ = __fmul2_rn(sq, w), sh = __fmul2_rn(sq, hh);
+    const float2 uv = __fmul2_rn(f2(su.x + su.y, sv.x + sv.y), f2b(di));
+    const float2 wh = __fmul2_rn(f2(sw_.x + sw_.y, sh.x + sh.y), f2b(di));
+    const float ut = uv.x, vt = uv.y, wt = wh.x, Ht = wh.y;
+    const float ke = 0.5f * (ut * ut + vt * vt + wt * wt);
+    const float a2 = gm1 * (Ht - ke);
+    const bool ok = (qL[0] > 0.0f) & (qR[0] > 0.0f) & (p.x > 0.0f) & (p.y > 0.0f) & (a2 > 0.0f);
+    const float ra = rsqrtf(a2);
+    const float a = a2 * ra;
+    const float rt = sq.x * sq.y;
+    const float unt = ut * nx + vt * ny + wt * nz;
+    const float dr = qR[0] - qL[0];
+    const float dp = p.y - p.x;
+    const float du = u.y - u.x, dv = v.y - v.x, dw = w.y - w.x;
+    const float dun = vn.y - vn.x;
+    // acoustic pair (l1, l4) with the Harten-Hyman fix
+    float2 l14 = __fadd2_rn(f2b(unt), f2(-a, a));
+    l14.x = fabsf(l14.x);
+    l14.y = fabsf(l14.y);
+    const float l2 = fabsf(unt);
+    const float delta = 0.05f * a;
+    const float idelta = (1.0f / 0.05f) * ra;
+    const float2 fix = __fmul2_rn(f2b(0.5f), __ffma2_rn(__fmul2_rn(l14, l14), f2b(idelta), f2b(delta)));
+    l14.x = l14.x < delta ? fix.x : l14.x;
+    l14.y = l14.y < delta ? fix.y : l14.y;
+    const float ia2h = 0.5f * ra * ra;
+    const float rad = rt * a * dun;
+    const float2 a14 = __fmul2_rn(__fadd2_rn(f2b(dp), f2(-rad, rad)), f2b(ia2h));
+    const float a2w = dr - dp * (ra * ra);
+    const float2 w14 = __fmul2_rn(l14, a14);
+    const float sw = w14.x + w14.y;
+    const float l2a2w = l2 * a2w;
+    const float l2rt = l2 * rt;
+    const float d0 = sw + l2a2w;
+    const float cn = (w14.y - w14.x) * a - l2rt * dun;
+    const float2 d12 = __ffma2_rn(f2b(l2rt), f2(du, dv), __ffma2_rn(f2b(cn), f2(nx, ny), __fmul2_rn(f2b(d0), uv)));
+    const float d3 = d0 * wt + cn * nz + l2rt * dw;
+    const float dE = sw * Ht + l2a2w * ke + cn * unt + l2rt * (ut * du + vt * dv + wt * dw);
+    const float ps = p.x + p.y;
+    // central part: qL vnL + qR vnR (+ p n) per variable, two variables per pair
+    const float2 c01 = __ffma2_rn(f2(qR[0], qR[1]), f2b(vn.y), __fmul2_rn(f2(qL[0], qL[1]), f2b(vn.x)));
+    const float2 c23 = __ffma2_rn(f2(qR[2], qR[3]), f2b(vn.y), __fmul2_rn(f2(qL[2], qL[3]), f2b(vn.x)));
+    const float c4 = (qL[4] + p.x) * vn.x + (qR[4] + p.y) * vn.y;
+    const float2 f01 = __fmul2_rn(f2b(0.5f), __fadd2_rn(__fadd2_rn(c01, f2(0.0f, ps * nx)), f2(-d0, -d12.x)));
+    const float2 f23 = __fmul2_rn(f2b(0.5f), __fadd2_rn(__ffma2_rn(f2b(ps), f2(ny, nz), c23), f2(-d12.y, -d3)));
+    f[0] = f01.x;
+    f[1] = f01.y;
+    f[2] = f23.x;
+    f[3] = f23.y;
+    f[4] = 0.5f * (c4 - dE);
+    return ok;
+}
+
 // local Lax-Friedrichs (Rusanov) flux
 template <typename T>
 __device__ __forceinline__ bool llf(const T qL[5], const T qR[5], const T n[3], T g, T f[5]) {

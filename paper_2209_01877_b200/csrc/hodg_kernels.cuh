@@ -278,6 +278,12 @@ constexpr bool FG4 = HODG_FACE_G4 && !HODG_FACE_CPASYNC;
 #ifndef HODG_FFMA2
 #define HODG_FFMA2 1
 #endif
+// FP32 Roe with the two sides in f32x2 lanes (roe_x2): measured off -- the
+// packing moves and horizontal sums eat the saved slots (P2 face 0.296 vs
+// 0.296 ms, P1 0.212 -> 0.217 ms)
+#ifndef HODG_ROE_X2
+#define HODG_ROE_X2 0
+#endif
 // phase-1 coefficient loads in pairs (one 16-byte / 8-byte shared load):
 // measured off -- FP64 P2 face 0.462 vs 0.463 ms, mixed 0.297 -> 0.304 ms
 #ifndef HODG_FACE_VEC
@@ -759,7 +765,12 @@ __global__ void __launch_bounds__(FACE_THREADS, (sizeof(T) == 4 ? HODG_FACE_MINB
             } else {
                 bool r[RP];
 #pragma unroll
-                for (int k = 0; k < RP; ++k) r[k] = roe(qL[k], qR[k], n[k], gam, h[k]);
+                for (int k = 0; k < RP; ++k) {
+                    if constexpr (sizeof(T) == 4 && HODG_ROE_X2)
+                        r[k] = roe_x2(qL[k], qR[k], n[k], gam, h[k]);
+                    else
+                        r[k] = roe(qL[k], qR[k], n[k], gam, h[k]);
+                }
 #pragma unroll
                 for (int k = 0; k < RP; ++k) ok[k] = ok[k] && r[k];
             }
