@@ -170,6 +170,10 @@ int hodg_face_flux_range32_es(const hodg_mesh* mesh, const float* state32, void*
 int hodg_local_dt(const hodg_mesh* mesh, const double* state, double cfl, double* dt_vec_out,
                   unsigned long long* dt_min, uint32_t* err, void* stream);
 int hodg_norm_finalize(const double* partial, int64_t n_blocks, double* out5, void* stream);
+/* Diagnostics (no reference counterpart): the last CUDA runtime / driver
+ * error code a kernel launcher saw, and where (*site: 1 shared-memory
+ * attribute, 2 tensor-map encode, 3 launch, 4 error after the launch). */
+int hodg_last_error(int* site);
 int hodg_residual_l2(const hodg_mesh* mesh, const double* res, double* scratch, double* out5, void* stream);
 int hodg_min_reduce_f64(const double* x, int64_t n, double* scratch, double* out, void* stream);
 int hodg_dt_fill(unsigned long long* slot, double value, void* stream);

@@ -98,6 +98,7 @@ SIGNATURES = {
     "hodg_halo_destroy": (I32, [P]),
     "hodg_local_dt": (I32, [P, P, D, P, P, P, P]),
     "hodg_norm_finalize": (I32, [P, I64, P, P]),
+    "hodg_last_error": (I32, [P]),
     "hodg_residual_l2": (I32, [P, P, P, P, P]),
     "hodg_min_reduce_f64": (I32, [P, I64, P, P, P]),
     "hodg_dt_fill": (I32, [P, D, P]),
@@ -167,7 +168,15 @@ def lib():
 
 def check(rc, what):
     if rc != HODG_OK:
-        raise HodgError(f"{what} failed with status {rc}")
+        detail = ""
+        if rc == HODG_ECUDA:
+            try:
+                site = C.c_int(0)
+                code = lib().hodg_last_error(C.byref(site))
+                detail = f" (CUDA error {code} at launcher site {site.value})"
+            except Exception:  # noqa: BLE001 -- diagnostics only
+                pass
+        raise HodgError(f"{what} failed with status {rc}{detail}")
 
 
 def ptr(t):

@@ -362,6 +362,18 @@ int hodg_modal_transform(const hodg_mesh* mesh, int to_reference, const double* 
     }
 }
 
+// last failing CUDA runtime / driver code seen by a kernel launcher and the
+// site (1 smem attribute, 2 tensor-map encode, 3 launch, 4 after launch)
+static int g_last_code = 0, g_last_site = 0;
+extern "C" void hodg_note_error(int code, int site) {
+    g_last_code = code;
+    g_last_site = site;
+}
+int hodg_last_error(int* site) {
+    if (site) *site = g_last_site;
+    return g_last_code;
+}
+
 int hodg_norm_finalize(const double* partial, int64_t n_blocks, double* out5, void* stream) {
     if (!partial || !out5 || n_blocks <= 0) return HODG_EINVAL;
     g_launches++;

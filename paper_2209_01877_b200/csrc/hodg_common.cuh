@@ -20,6 +20,10 @@
 
 #define HODG_ERR_NONE 0xFFFFFFFFu
 
+// diagnostics: the last failing CUDA / driver code seen by a launcher and
+// where (hodg_last_error in hodg_abi.cu); launchers return HODG_ECUDA
+extern "C" void hodg_note_error(int code, int site);
+
 namespace hodg {
 
 // ---------------------------------------------------------------------------
@@ -89,6 +93,9 @@ __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* tm, in
 // 4-byte, `cols * elem` a multiple of 16 bytes) for tma_gather4: box = one
 // full row.  The row count is left open (2^31 - 1): the kernels index only
 // valid rows or -1.
+#ifndef HODG_G4_ROWS
+#define HODG_G4_ROWS 0x7FFFFFFF
+#endif
 #ifndef HODG_G4_PROMOTION
 #define HODG_G4_PROMOTION CU_TENSOR_MAP_L2_PROMOTION_NONE
 #endif
@@ -101,7 +108,7 @@ static inline int encode_row_map(CUtensorMap* tm, const void* base, int cols, in
             q != cudaDriverEntryPointSuccess || !enc)
             return HODG_ECUDA;
     }
-    const cuuint64_t gdim[2] = {cuuint64_t(cols), cuuint64_t(0x7FFFFFFF)};
+    const cuuint64_t gdim[2] = {cuuint64_t(cols), cuuint64_t(HODG_G4_ROWS)};
     const cuuint64_t gstride[1] = {cuuint64_t(cols) * elem_bytes};
     const cuuint32_t box[2] = {cuuint32_t(cols), 1};
     const cuuint32_t es[2] = {1, 1};
@@ -109,6 +116,7 @@ static inline int encode_row_map(CUtensorMap* tm, const void* base, int cols, in
                            const_cast<void*>(base), gdim, gstride, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                            CU_TENSOR_MAP_SWIZZLE_NONE, HODG_G4_PROMOTION,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) hodg_note_error(int(r), 2);
     return r == CUDA_SUCCESS ? HODG_OK : HODG_ECUDA;
 }
 

@@ -264,15 +264,24 @@ __host__ __device__ constexpr int expt(int i, int d) {
 #endif
 constexpr int FNBUF = HODG_FACE_NBUF;
 // state rows by TMA tile::gather4: four (face, side) rows per instruction
-// (one per row otherwise); rows land in 128-byte-aligned groups of four
+// (one per row otherwise); rows land in 128-byte-aligned groups of four.
+// Off: faster (FP64 P2 face 0.489 -> 0.475 ms, mixed 0.334 -> 0.322 ms) and
+// parity-green in isolation, but one GPU-suite ordering (the 2D, halo and
+// multi-rank tests before the parity tests) hits an illegal-address fault in
+// the P1 face launch with it, reproducibly, and never without it; the cause
+// is not found, so the shipped default is the per-row
+// bulk copy
 #ifndef HODG_FACE_G4
-#define HODG_FACE_G4 1
+#define HODG_FACE_G4 0
 #endif
 constexpr bool FG4 = HODG_FACE_G4 && !HODG_FACE_CPASYNC;
 // phase-1 traces without per-qp branches or zero-initialised accumulators
 // (1: except FP64 P3, where it measured 0.704 -> 0.750 ms; 2: everywhere)
 #ifndef HODG_FACE_P1_FLAT
 #define HODG_FACE_P1_FLAT 1
+#endif
+#ifndef HODG_TM_FENCE
+#define HODG_TM_FENCE 0
 #endif
 // FP32 contractions as packed f32x2 FMAs (FFMA2: two FMAs per issue slot)
 #ifndef HODG_FFMA2
@@ -572,6 +581,13 @@ __global__ void __launch_bounds__(FACE_THREADS, (sizeof(T) == 4 ? HODG_FACE_MINB
 
     int tile = blockIdx.x;
     Meta cur = load_meta(tile);
+#if HODG_TM_FENCE
+    if constexpr (FG4) {
+        // make the TMA unit see this launch's row map (a descriptor cached
+        // from an earlier launch at the same parameter address would be stale)
+        asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(&rmap) : "memory");
+    }
+#endif
     __syncthreads();  // barrier init visible
     // programmatic dependent launch: the prologue above (barriers, face
     // table, first metadata) overlapped the previous kernel's tail; its state
@@ -1506,8 +1522,11 @@ static int launch_setup(LaunchCache& lc, K kernel, int threads, size_t smem, int
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return HODG_ECUDA;
     if (lc.cap[dev] == 0) {
-        if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
+        const cudaError_t ae = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (ae != cudaSuccess) {
+            hodg_note_error(int(ae), 1);
             return HODG_ECUDA;
+        }
         int sms = 0, per_sm = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
@@ -1534,11 +1553,17 @@ static int launch_maybe_pdl(const hodg_mesh_desc& m, K kernel, int64_t nblk, int
         at[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        if (cudaLaunchKernelEx(&cfg, kernel, args...) != cudaSuccess) return HODG_ECUDA;
+        const cudaError_t le = cudaLaunchKernelEx(&cfg, kernel, args...);
+        if (le != cudaSuccess) {
+            hodg_note_error(int(le), 3);
+            return HODG_ECUDA;
+        }
     } else {
         kernel<<<unsigned(nblk), threads, smem, st>>>(args...);
     }
-    return cudaGetLastError() == cudaSuccess ? HODG_OK : HODG_ECUDA;
+    const cudaError_t ge = cudaGetLastError();
+    if (ge != cudaSuccess) hodg_note_error(int(ge), 4);
+    return ge == cudaSuccess ? HODG_OK : HODG_ECUDA;
 }
 
 template <typename T, bool BND, bool ES, typename R>
