@@ -338,9 +338,11 @@ constexpr bool EPERSIST = HODG_EPERSIST && !WARP_ELEM && ORDER <= 2 && H == 1;
 // face-ordered records by TMA tile::gather4 (four records per instruction),
 // in 128-byte-aligned groups of four.  1: FP64 (P0 / P1 / P2 element kernel
 // 0.128 / 0.252 / 0.464 -> 0.109 / 0.240 / 0.444 ms at C1M); 2: also FP32,
-// whose groups put a warp's record reads on few banks (P2 0.345 -> 0.388 ms)
+// whose groups put a warp's record reads on few banks (P2 0.345 -> 0.388 ms).
+// Off by default, as HODG_FACE_G4: with gather4 in the kernels the full GPU
+// suite hit an illegal-address fault in 2 of 7 runs (never without it)
 #ifndef HODG_ELEM_G4
-#define HODG_ELEM_G4 1
+#define HODG_ELEM_G4 0
 #endif
 template <typename T>
 __host__ __device__ constexpr bool elem_g4() {
