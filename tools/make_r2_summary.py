@@ -42,8 +42,9 @@ def full(rep):
 def main():
     out = ["# ncu summary, round 2 (C1M P2, `bench.py --no-cpu --no-sub --steps 5 --warmup 3`)\n",
            "Captured on the B200 after the round-2 kernel changes (flux-moment volume integral, exact face-gather "
-           "folding, regrouped Roe dissipation, FP32 state shadow in mixed precision, TMA tile::gather4 for the face "
-           "kernel's state rows and the FP64 element kernel's face records, branch-free face traces). "
+           "folding, regrouped Roe dissipation, FP32 state shadow in mixed precision, branch-free face traces, packed "
+           "FP32 (FFMA2) contractions in the mixed kernels, cp.async FP32 face records; state rows and FP64 records by "
+           "per-row TMA bulk copies -- the gather4 variants are off by default, DESIGN.md section 3). "
            "Commands: `tools/profile_r2.sh`, `tools/profile_elem.sh`.\n",
            "## Launch list (gpu__time_duration.sum, cold-cache, serialised; whole bench process incl. setup)\n"]
     rows = list(csv.reader(open(os.path.join(GO, "r2p_launches.csv"))))
