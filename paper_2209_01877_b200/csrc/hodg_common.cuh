@@ -99,7 +99,8 @@ __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* tm, in
 #ifndef HODG_G4_PROMOTION
 #define HODG_G4_PROMOTION CU_TENSOR_MAP_L2_PROMOTION_NONE
 #endif
-static inline int encode_row_map(CUtensorMap* tm, const void* base, int cols, int elem_bytes) {
+static inline int encode_row_map(CUtensorMap* tm, const void* base, int cols, int elem_bytes,
+                                 uint64_t rows = HODG_G4_ROWS) {
     static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
     if (!enc) {
         cudaDriverEntryPointQueryResult q;
@@ -108,7 +109,7 @@ static inline int encode_row_map(CUtensorMap* tm, const void* base, int cols, in
             q != cudaDriverEntryPointSuccess || !enc)
             return HODG_ECUDA;
     }
-    const cuuint64_t gdim[2] = {cuuint64_t(cols), cuuint64_t(HODG_G4_ROWS)};
+    const cuuint64_t gdim[2] = {cuuint64_t(cols), cuuint64_t(rows)};
     const cuuint64_t gstride[1] = {cuuint64_t(cols) * elem_bytes};
     const cuuint32_t box[2] = {cuuint32_t(cols), 1};
     const cuuint32_t es[2] = {1, 1};

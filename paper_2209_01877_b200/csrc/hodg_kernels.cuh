@@ -280,6 +280,12 @@ constexpr bool FG4 = HODG_FACE_G4 && !HODG_FACE_CPASYNC;
 #ifndef HODG_FACE_P1_FLAT
 #define HODG_FACE_P1_FLAT 1
 #endif
+#ifndef HODG_G4_EXACT
+#define HODG_G4_EXACT 0  // debug: the row map's extent = n_elems (ghost rows would read as zeros)
+#endif
+#ifndef HODG_G4_DEBUG
+#define HODG_G4_DEBUG 0
+#endif
 #ifndef HODG_TM_FENCE
 #define HODG_TM_FENCE 0
 #endif
@@ -552,6 +558,21 @@ __global__ void __launch_bounds__(FACE_THREADS, (sizeof(T) == 4 ? HODG_FACE_MINB
             const int e2 = __shfl_down_sync(0xffffffffu, mt.elem, 2 * NG);
             const int e3 = __shfl_down_sync(0xffffffffu, mt.elem, 3 * NG);
             if (g == 0 && (lf & 3) == 0) {
+#if HODG_G4_DEBUG
+                {
+                    const int lim = int(2 * m.n_faces);  // (ghost rows sit past n_elems)
+                    const bool bad_idx = mt.elem < -1 || mt.elem >= lim || e1 < -1 || e1 >= lim || e2 < -1 ||
+                                         e2 >= lim || e3 < -1 || e3 >= lim;
+                    const bool bad_dst = (smem_u32(row) & 127u) != 0;
+                    const bool bad_map = (reinterpret_cast<uintptr_t>(&rmap) & 63u) != 0;
+                    if (bad_idx || bad_dst || bad_map) {
+                        printf("G4DBG blk %d side %d lf %d idx %d %d %d %d lim %d dst %u map %p f0 %lld fe %lld\n",
+                               int(blockIdx.x), side, lf, mt.elem, e1, e2, e3, lim, smem_u32(row),
+                               (const void*)&rmap, (long long)f_begin, (long long)f_end);
+                        __trap();
+                    }
+                }
+#endif
                 mbar_arrive_expect_tx(bar + buf, 4 * RR * sizeof(R));
                 tma_gather4(row, &rmap, mt.elem, e1, e2, e3, bar + buf);
             } else {
@@ -1578,7 +1599,10 @@ static int launch_face_k(const hodg_mesh_desc& m, const R* state, void* hbuf, ui
     const int64_t ntiles = (fe - fb + FT - 1) / FT;
     const int64_t nblk = ntiles < cap ? ntiles : cap;  // persistent CTAs loop over tiles
     CUtensorMap rmap = {};
-    if (FG4 && nblk > 0 && encode_row_map(&rmap, state, rstride<R>(), int(sizeof(R))) != HODG_OK) return HODG_ECUDA;
+    if (FG4 && nblk > 0 &&
+        encode_row_map(&rmap, state, rstride<R>(), int(sizeof(R)),
+                       HODG_G4_EXACT ? uint64_t(m.n_elems) : uint64_t(HODG_G4_ROWS)) != HODG_OK)
+        return HODG_ECUDA;
     return launch_maybe_pdl(m, face_flux_kernel<T, BND, ES, R>, nblk, FACE_THREADS, sm, st, m, state,
                             static_cast<T*>(hbuf), err, fb, fe, rmap);
 }
